@@ -1,0 +1,167 @@
+/*
+ * gmsketch_b200.h -- C ABI of the B200-native FastGM engine
+ * (libgmsketch_b200.so, built for sm_100a).
+ *
+ * The reference (gmsketch 0.1.0, /root/reference/pkg/src/gmsketch) is pure
+ * Python and has no FFI; its "operator API" is the Python function surface
+ * of gmsketch/__init__.py:12-109.  Each entry point below names the
+ * reference function(s) it replaces; the Python host package
+ * paper_2302_05176_b200 binds them with ctypes and re-exports the
+ * reference names.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Pointers marked (device) must be CUDA
+ *    device (or managed) memory; (host) pointers may be pageable or pinned.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *  - Element ids are unsigned 32- or 64-bit (id_bits = 32 | 64).  The
+ *    reference keys its RNG on the id modulo 2**64 (randgen.py:115), so a
+ *    negative Python id e is passed as e mod 2**64.
+ *  - Weights are IEEE float or double (w_bits = 32 | 64); float weights are
+ *    widened exactly to double, like float(np.float32(x)) in the reference.
+ *  - Sketch registers: y (double, the value min_i E_ij / v_i) and s (uint64
+ *    element id), k per sketch, row-major for batches.  An unset register
+ *    has y = +inf and s = UINT64_MAX.
+ *  - Return value: GM_OK (0) or one of the error codes below, which map 1:1
+ *    onto the reference exception classes (errors.py:4-58); gm_last_error()
+ *    returns a thread-local message for the last failing call.
+ *  - Unless GM_FLAG_ASYNC is set, a call synchronises `stream` before it
+ *    returns and reports data errors (bad weights, empty vectors).  With
+ *    GM_FLAG_ASYNC the call only enqueues work; data errors are latched on
+ *    the stream and returned by gm_stream_status().
+ *  - Re-entrant per stream: scratch is kept per (device, stream); calls on
+ *    different streams may run concurrently.
+ */
+#ifndef GMSKETCH_B200_H
+#define GMSKETCH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error codes (reference exception in parentheses) */
+#define GM_OK 0
+#define GM_ERR_EMPTY_VECTOR 1       /* EmptyVectorError        sketch.py:172-174   */
+#define GM_ERR_INVALID_WEIGHT 2     /* InvalidWeightError      sketch.py:54-64     */
+#define GM_ERR_INVALID_PARAMETER 3  /* InvalidParameterError   sketch.py:151-157   */
+#define GM_ERR_INCONSISTENT_WEIGHT 4 /* InconsistentWeightError stream.py:67-73    */
+#define GM_ERR_INCOMPLETE 5         /* IncompleteSketchError   stream.py:132-134   */
+#define GM_ERR_MISMATCHED 6         /* MismatchedSketchError   sketch.py:314-322   */
+#define GM_ERR_CUDA 100             /* CUDA runtime failure (no reference class)   */
+#define GM_ERR_NO_DEVICE 101        /* no sm_100 device visible                     */
+
+/* flags */
+#define GM_FLAG_ASYNC 0x1u       /* enqueue only; see gm_stream_status()           */
+#define GM_FLAG_EXHAUSTIVE 0x2u  /* run every queue to k (sketch_naive semantics)  */
+#define GM_FLAG_ACCUMULATE 0x4u  /* gm_sketch_elements: fold into y_io/s_io        */
+
+/* Library version (major*10000 + minor*100 + patch). */
+int gm_version(void);
+/* Thread-local message of the last failing call ("" if none). */
+const char *gm_last_error(void);
+/* Returns and clears the data error latched on `stream` by GM_FLAG_ASYNC
+ * calls; synchronises the stream. */
+int gm_stream_status(void *stream);
+
+/*
+ * Batch of independent CSR vectors -> n_vec sketches.
+ * Replaces sketch_fast / sketch_fast_counted (sketch.py:212-311) and, with
+ * GM_FLAG_EXHAUSTIVE, sketch_naive / sketch_naive_counted (sketch.py:177-209),
+ * applied to each vector; the reference has no batch call (its callers
+ * loop, e.g. bench.py:264-292).
+ *   ids, w      (device) n = offsets[n_vec] elements; ids distinct within a
+ *               vector (WeightedVector keys, sketch.py:50-68)
+ *   offsets     (device) n_vec+1 int64 CSR offsets
+ *   y_out,s_out (device) n_vec*k
+ *   emitted_out (device, nullable) n_vec arrivals computed per vector (the
+ *               work counter of the *_counted variants; schedule-dependent)
+ * Errors: GM_ERR_INVALID_PARAMETER (k outside [1, 65536], bad bits),
+ *         GM_ERR_INVALID_WEIGHT, GM_ERR_EMPTY_VECTOR (a vector with no
+ *         elements).
+ */
+int gm_sketch_csr(const void *ids, int id_bits, const void *w, int w_bits,
+                  const int64_t *offsets, int64_t n_vec, int32_t k,
+                  uint64_t global_seed, uint64_t stream_salt, uint32_t flags,
+                  double *y_out, uint64_t *s_out, int64_t *emitted_out,
+                  void *stream);
+
+/* Same contract with HOST buffers; copies in and out inside the call. */
+int gm_sketch_csr_host(const void *ids, int id_bits, const void *w, int w_bits,
+                       const int64_t *offsets, int64_t n_vec, int32_t k,
+                       uint64_t global_seed, uint64_t stream_salt,
+                       uint32_t flags, double *y_out, uint64_t *s_out,
+                       int64_t *emitted_out, void *stream);
+
+/*
+ * One sketch over a large element set: a huge vector, or an (id, weight)
+ * stream in which an id may repeat with the SAME weight (a repeat is a no-op
+ * on the registers, stream.py:74-78).
+ * Replaces sketch_stream / stream_update / stream_finalize
+ * (stream.py:58-153) for bulk input and sketch_fast for vectors too large
+ * for one CTA.
+ *   ids, w      (device) n elements
+ *   y_io, s_io  (device) k registers; read first when GM_FLAG_ACCUMULATE
+ *   emitted_out (host, nullable) arrivals computed
+ * Errors: GM_ERR_INVALID_PARAMETER, GM_ERR_INVALID_WEIGHT,
+ *         GM_ERR_INCOMPLETE (n == 0 and no accumulated registers).
+ * Always synchronises `stream` (the pass count is data-dependent).
+ */
+int gm_sketch_elements(const void *ids, int id_bits, const void *w, int w_bits,
+                       int64_t n, int32_t k, uint64_t global_seed,
+                       uint64_t stream_salt, uint32_t flags, double *y_io,
+                       uint64_t *s_io, int64_t *emitted_out, void *stream);
+
+/* Same contract with HOST buffers. */
+int gm_sketch_elements_host(const void *ids, int id_bits, const void *w,
+                            int w_bits, int64_t n, int32_t k,
+                            uint64_t global_seed, uint64_t stream_salt,
+                            uint32_t flags, double *y_io, uint64_t *s_io,
+                            int64_t *emitted_out, void *stream);
+
+/*
+ * Per-register minimum over n_sk sketches (row-major y_in/s_in, device),
+ * strict '<' so the earlier sketch wins exact ties.  Replaces merge
+ * (estimate.py:103-125); k/fingerprint compatibility (sketch.py:314-322) is
+ * the caller's check.
+ */
+int gm_merge(const double *y_in, const uint64_t *s_in, int64_t n_sk,
+             int32_t k, double *y_out, uint64_t *s_out, void *stream);
+
+/*
+ * Register-match counts of n_pairs sketch pairs (device, row-major
+ * n_pairs*k): matches[p] = #{j : s_a[p,j] == s_b[p,j]}.  The numerator of
+ * estimate_jaccard_p (estimate.py:47-55); the estimate is matches/k.
+ */
+int gm_match_count(const uint64_t *s_a, const uint64_t *s_b, int64_t n_pairs,
+                   int32_t k, int32_t *matches, void *stream);
+
+/* K0 test surface (device arrays of length n): uniform_open
+ * (randgen.py:107-119) and the permutation draw j in [z, k]
+ * (rand_int_between(scheme, e, z, z, k), randgen.py:122-143). */
+int gm_uniform_open_batch(const uint64_t *global_seeds, const uint64_t *elements,
+                          const uint64_t *steps, int64_t n, double *out,
+                          void *stream);
+int gm_perm_draw_batch(const uint64_t *perm_seeds, const uint64_t *elements,
+                       const uint64_t *steps, const uint32_t *ks, int64_t n,
+                       uint32_t *out, void *stream);
+
+/* Diagnostics.
+ * gm_probe_arrival_rate: n_threads threads each emit `iters` exact arrivals
+ * (spacing + permutation draw, no pruning or registers); the measured rate
+ * is the compute roofline of the sketch kernels.  sink: 1
+ * device double.  Asynchronous.
+ * gm_count_arrivals_csr: counts[v] = number of arrivals t <= tau[v] over the
+ * elements of CSR vector v (device arrays); the algorithmic survivor count.
+ * Synchronises `stream`. */
+int gm_probe_arrival_rate(int64_t n_threads, int32_t iters, int32_t k,
+                          double *sink, void *stream);
+int gm_count_arrivals_csr(const void *ids, int id_bits, const void *w,
+                          int w_bits, const int64_t *offsets, int64_t n_vec,
+                          int32_t k, uint64_t global_seed, const double *tau,
+                          unsigned long long *counts, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GMSKETCH_B200_H */

@@ -1,0 +1,516 @@
+// gm_capi.cu -- the C ABI (include/gmsketch_b200.h) over the sm_100a kernels.
+//
+// Host orchestration only: argument checks, per-(device, stream) scratch,
+// launch configuration, the pass loop of gm_sketch_elements, error mapping.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
+
+#include "../../include/gmsketch_b200.h"
+#include "gm_kernels.cuh"
+
+using namespace gmk;
+
+namespace {
+
+thread_local char g_msg[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_msg, sizeof(g_msg), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(GM_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));       \
+  } while (0)
+
+struct Workspace {
+  int* counters = nullptr;                 // [0] vector ticket, [1] unset registers
+  unsigned long long* err = nullptr;       // latched data error
+  unsigned long long* ull = nullptr;       // [0] heavy count, [1] emitted total
+  double* dbl = nullptr;                   // [0] tau, [1] weight sample sum
+  unsigned long long* host = nullptr;      // pinned readback (4 words)
+  Reg* regs = nullptr;
+  size_t regs_cap = 0;
+  u64* heavy = nullptr;
+  size_t heavy_cap = 0;
+  u32* dense = nullptr;
+  size_t dense_cap = 0;
+  void* stage = nullptr;                   // device staging for *_host calls
+  size_t stage_cap = 0;
+};
+
+std::mutex g_mu;
+std::map<std::pair<int, cudaStream_t>, Workspace*> g_ws;
+
+int get_ws(cudaStream_t st, Workspace** out) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_pair(dev, st);
+  auto it = g_ws.find(key);
+  if (it != g_ws.end()) {
+    *out = it->second;
+    return GM_OK;
+  }
+  int major = 0;
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major < 10) return fail(GM_ERR_NO_DEVICE, "device %d is sm_%d0; this library targets sm_100a", dev, major);
+  Workspace* w = new Workspace();
+  CK(cudaMalloc(&w->counters, 4 * sizeof(int)));
+  CK(cudaMalloc(&w->err, sizeof(unsigned long long)));
+  CK(cudaMalloc(&w->ull, 4 * sizeof(unsigned long long)));
+  CK(cudaMalloc(&w->dbl, 4 * sizeof(double)));
+  CK(cudaMallocHost(&w->host, 4 * sizeof(unsigned long long)));
+  CK(cudaMemset(w->counters, 0, 4 * sizeof(int)));
+  CK(cudaMemset(w->err, 0, sizeof(unsigned long long)));
+  CK(cudaDeviceSynchronize());
+  g_ws[key] = w;
+  *out = w;
+  return GM_OK;
+}
+
+template <class T>
+int grow(T** p, size_t* cap, size_t need, cudaStream_t st, bool zero = false) {
+  if (*cap >= need) return GM_OK;
+  if (*p) CK(cudaFreeAsync(*p, st));
+  size_t n = need + need / 4;
+  CK(cudaMallocAsync((void**)p, n * sizeof(T), st));
+  if (zero) CK(cudaMemsetAsync(*p, 0, n * sizeof(T), st));
+  *cap = n;
+  return GM_OK;
+}
+
+int map_device_error(unsigned long long e) {
+  const int code = (int)(e & 0xFFFFFFFFull);
+  const unsigned long long where = e >> 32;
+  switch (code) {
+    case GM_ERR_EMPTY_VECTOR:
+      return fail(code, "EmptyVectorError: vector %llu has no positive entries", where);
+    case GM_ERR_INVALID_WEIGHT:
+      return fail(code, "InvalidWeightError: weight not finite, > 0 and >= 1e-300 (vector/element %llu)", where);
+    default:
+      return fail(code, "device error %d at %llu", code, where);
+  }
+}
+
+// reads and clears the latched error word; synchronises st
+int check_sync(Workspace* ws, cudaStream_t st) {
+  CK(cudaMemcpyAsync(ws->host, ws->err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  const unsigned long long e = ws->host[0];
+  if (e) {
+    CK(cudaMemsetAsync(ws->err, 0, sizeof(unsigned long long), st));
+    CK(cudaStreamSynchronize(st));
+    return map_device_error(e);
+  }
+  return GM_OK;
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+size_t csr_smem_bytes(u32 k) {
+  const size_t pool = k <= DENSE_SMEM_MAX_K ? std::max((size_t)LIGHT_CAP * NT, (size_t)NWARP * k)
+                                            : (size_t)LIGHT_CAP * NT;
+  return (size_t)k * sizeof(Reg) + pool * 4 + NWARP * 32 * 8 + NWARP * 32 * 4 + HEAVY_LIST * 4;
+}
+
+template <class IdT, class WT>
+int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k,
+               u64 useed, u64 pseed, double* y, u64* s, int64_t* em, Workspace* ws,
+               cudaStream_t st, int attempt0) {
+  auto kern = csr_sketch_kernel<IdT, WT>;
+  const size_t smem = csr_smem_bytes(k);
+  int per_sm = 0;
+  {
+    // occupancy per (kernel, smem) is cached: the launch path stays a
+    // memset + one kernel launch
+    static std::mutex mu;
+    static std::map<std::pair<const void*, size_t>, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair((const void*)kern, smem);
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+      if (smem <= 232448) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+      }
+      it = cache.emplace(key, per_sm).first;
+    }
+    per_sm = it->second;
+  }
+  if (per_sm < 1) return -1;  // registers do not fit in shared memory: caller falls back
+  int64_t grid = (int64_t)per_sm * num_sms();
+  if (grid > n_vec) grid = n_vec;
+  u32* dense = nullptr;
+  if (k > DENSE_SMEM_MAX_K) {
+    int rc = grow(&ws->dense, &ws->dense_cap, (size_t)grid * NWARP * k, st);
+    if (rc) return rc;
+    dense = ws->dense;
+  }
+  CK(cudaMemsetAsync(ws->counters, 0, sizeof(int), st));
+  kern<<<(unsigned)grid, NT, smem, st>>>((const IdT*)ids, (const WT*)w, offsets, n_vec, k, useed,
+                                         pseed, y, s, em, ws->counters, dense, ws->err, attempt0);
+  CK(cudaGetLastError());
+  return GM_OK;
+}
+
+int check_common(int id_bits, int w_bits, int32_t k) {
+  if (id_bits != 32 && id_bits != 64) return fail(GM_ERR_INVALID_PARAMETER, "id_bits must be 32 or 64, got %d", id_bits);
+  if (w_bits != 32 && w_bits != 64) return fail(GM_ERR_INVALID_PARAMETER, "w_bits must be 32 or 64, got %d", w_bits);
+  if (k < 1) return fail(GM_ERR_INVALID_PARAMETER, "InvalidParameterError: k must be >= 1, got %d", k);
+  if (k > 65536) return fail(GM_ERR_INVALID_PARAMETER, "k=%d exceeds the supported maximum 65536", k);
+  return GM_OK;
+}
+
+template <class IdT, class WT>
+int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u64 pseed,
+                 uint32_t flags, double* y_io, u64* s_io, int64_t* emitted_out, Workspace* ws,
+                 cudaStream_t st) {
+  int rc = grow(&ws->regs, &ws->regs_cap, (size_t)k, st);
+  if (rc) return rc;
+  CK(cudaMemsetAsync(ws->counters, 0, 4 * sizeof(int), st));
+  CK(cudaMemsetAsync(ws->ull, 0, 4 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(ws->dbl, 0, 4 * sizeof(double), st));
+  const unsigned rgrid = (k + 255) / 256;
+  if (flags & GM_FLAG_ACCUMULATE)
+    load_regs_kernel<<<rgrid, 256, 0, st>>>(ws->regs, k, y_io, s_io, ws->counters + 1);
+  else
+    init_regs_kernel<<<rgrid, 256, 0, st>>>(ws->regs, k, ws->counters + 1);
+  CK(cudaGetLastError());
+  if (n > 0) {
+    const int64_t sample = 1 << 20;
+    const int64_t step = n > sample ? n / sample : 1;
+    weight_sample_kernel<WT><<<256, 256, 0, st>>>((const WT*)w, n, step, ws->dbl + 1);
+    CK(cudaGetLastError());
+    const int64_t heavy_need = std::min<int64_t>(n, (int64_t)1 << 22);
+    rc = grow(&ws->heavy, &ws->heavy_cap, (size_t)heavy_need, st);
+    if (rc) return rc;
+    const int64_t heavy_blocks = (int64_t)num_sms() * 4;
+    rc = grow(&ws->dense, &ws->dense_cap, (size_t)heavy_blocks * NWARP * k, st, true);
+    if (rc) return rc;
+    int light_per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&light_per_sm, elem_light_kernel<IdT, WT>, NT, 0));
+    int64_t lgrid = (int64_t)light_per_sm * num_sms();
+    lgrid = std::min<int64_t>(lgrid, (n + NT - 1) / NT);
+    for (int attempt = 0;; ++attempt) {
+      tau_kernel<<<1, 1, 0, st>>>(ws->dbl, ws->dbl + 1, k, (flags & GM_FLAG_EXHAUSTIVE) ? 5 : attempt,
+                                  ws->counters + 1);
+      CK(cudaMemsetAsync(ws->ull, 0, sizeof(unsigned long long), st));
+      elem_light_kernel<IdT, WT><<<(unsigned)lgrid, NT, 0, st>>>(
+          (const IdT*)ids, (const WT*)w, n, k, useed, pseed, ws->dbl, ws->regs, ws->counters + 1,
+          ws->heavy, (int64_t)ws->heavy_cap, ws->ull, emitted_out ? ws->ull + 1 : nullptr, ws->err);
+      CK(cudaGetLastError());
+      elem_heavy_kernel<IdT, WT><<<(unsigned)heavy_blocks, NT, 0, st>>>(
+          (const IdT*)ids, (const WT*)w, k, useed, pseed, ws->dbl, ws->regs, ws->counters + 1,
+          ws->heavy, ws->ull, (int64_t)ws->heavy_cap, ws->dense,
+          emitted_out ? ws->ull + 1 : nullptr);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(ws->host, ws->counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(ws->host + 1, ws->ull, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      const int unset = (int)(ws->host[0] & 0xFFFFFFFFull);
+      const unsigned long long nheavy = ws->host[1];
+      if (nheavy > ws->heavy_cap)
+        return fail(GM_ERR_CUDA, "internal: heavy-element list overflow (%llu > %zu)", nheavy, ws->heavy_cap);
+      if (unset == 0 || (flags & GM_FLAG_EXHAUSTIVE) || attempt >= 5) break;
+    }
+  }
+  store_regs_kernel<<<rgrid, 256, 0, st>>>(ws->regs, k, y_io, s_io);
+  CK(cudaGetLastError());
+  if (emitted_out) CK(cudaMemcpyAsync(ws->host + 2, ws->ull + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ws->host, ws->counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  rc = check_sync(ws, st);
+  if (rc) return rc;
+  if (emitted_out) *emitted_out = (int64_t)ws->host[2];
+  return GM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gm_version(void) { return 100; }
+
+const char* gm_last_error(void) { return g_msg; }
+
+int gm_stream_status(void* stream) {
+  Workspace* ws = nullptr;
+  int rc = get_ws((cudaStream_t)stream, &ws);
+  if (rc) return rc;
+  return check_sync(ws, (cudaStream_t)stream);
+}
+
+int gm_sketch_elements(const void* ids, int id_bits, const void* w, int w_bits, int64_t n,
+                       int32_t k, uint64_t global_seed, uint64_t stream_salt, uint32_t flags,
+                       double* y_io, uint64_t* s_io, int64_t* emitted_out, void* stream);
+
+// k too large for shared-memory registers: one grid-wide sketch per vector
+static int csr_by_elements(const void* ids, int id_bits, const void* w, int w_bits,
+                           const int64_t* offsets, int64_t n_vec, int32_t k, uint64_t seed,
+                           uint64_t salt, uint32_t flags, double* y_out, uint64_t* s_out,
+                           int64_t* emitted_out, cudaStream_t st) {
+  int64_t* off = (int64_t*)malloc((size_t)(n_vec + 1) * 8);
+  if (!off) return fail(GM_ERR_CUDA, "host allocation failed");
+  cudaError_t e = cudaMemcpyAsync(off, offsets, (size_t)(n_vec + 1) * 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    free(off);
+    return fail(GM_ERR_CUDA, "offsets readback failed: %s", cudaGetErrorString(e));
+  }
+  int rc = GM_OK;
+  for (int64_t v = 0; v < n_vec && rc == GM_OK; ++v) {
+    const int64_t lo = off[v], n = off[v + 1] - lo;
+    if (n == 0) {
+      rc = fail(GM_ERR_EMPTY_VECTOR, "EmptyVectorError: vector %lld has no positive entries", (long long)v);
+      break;
+    }
+    int64_t em = 0;
+    rc = gm_sketch_elements((const char*)ids + lo * (id_bits / 8), id_bits,
+                            (const char*)w + lo * (w_bits / 8), w_bits, n, k, seed, salt,
+                            flags & GM_FLAG_EXHAUSTIVE, y_out + v * (int64_t)k, s_out + v * (int64_t)k,
+                            emitted_out ? &em : nullptr, st);
+    if (rc == GM_OK && emitted_out) {
+      cudaError_t e2 = cudaMemcpyAsync(emitted_out + v, &em, 8, cudaMemcpyHostToDevice, st);
+      if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(st);
+      if (e2 != cudaSuccess) rc = fail(GM_ERR_CUDA, "%s", cudaGetErrorString(e2));
+    }
+  }
+  free(off);
+  return rc;
+}
+
+int gm_sketch_csr(const void* ids, int id_bits, const void* w, int w_bits, const int64_t* offsets,
+                  int64_t n_vec, int32_t k, uint64_t global_seed, uint64_t stream_salt,
+                  uint32_t flags, double* y_out, uint64_t* s_out, int64_t* emitted_out,
+                  void* stream) {
+  g_msg[0] = 0;
+  int rc = check_common(id_bits, w_bits, k);
+  if (rc) return rc;
+  if (n_vec < 0) return fail(GM_ERR_INVALID_PARAMETER, "n_vec must be >= 0");
+  if (n_vec == 0) return GM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace* ws = nullptr;
+  rc = get_ws(st, &ws);
+  if (rc) return rc;
+  const u64 useed = global_seed;
+  const u64 pseed = global_seed ^ stream_salt;
+  const u32 kk = (u32)k;
+  // exhaustive = a single pass with tau = +inf (pass_tau's last attempt)
+  const int a0 = (flags & GM_FLAG_EXHAUSTIVE) ? 3 : 0;
+  if (id_bits == 32 && w_bits == 32)
+    rc = launch_csr<u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
+  else if (id_bits == 32)
+    rc = launch_csr<u32, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
+  else if (w_bits == 32)
+    rc = launch_csr<u64, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
+  else
+    rc = launch_csr<u64, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
+  if (rc == -1) return csr_by_elements(ids, id_bits, w, w_bits, offsets, n_vec, k, global_seed,
+                                       stream_salt, flags, y_out, s_out, emitted_out, st);
+  if (rc) return rc;
+  if (flags & GM_FLAG_ASYNC) return GM_OK;
+  return check_sync(ws, st);
+}
+
+int gm_sketch_csr_host(const void* ids, int id_bits, const void* w, int w_bits,
+                       const int64_t* offsets, int64_t n_vec, int32_t k, uint64_t global_seed,
+                       uint64_t stream_salt, uint32_t flags, double* y_out, uint64_t* s_out,
+                       int64_t* emitted_out, void* stream) {
+  g_msg[0] = 0;
+  int rc = check_common(id_bits, w_bits, k);
+  if (rc) return rc;
+  if (n_vec < 0) return fail(GM_ERR_INVALID_PARAMETER, "n_vec must be >= 0");
+  if (n_vec == 0) return GM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace* ws = nullptr;
+  rc = get_ws(st, &ws);
+  if (rc) return rc;
+  const int64_t n = offsets[n_vec];
+  const size_t ib = (size_t)n * (id_bits / 8), wb = (size_t)n * (w_bits / 8);
+  const size_t ob = (size_t)(n_vec + 1) * 8, yb = (size_t)n_vec * k * 8;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t need = al(ib) + al(wb) + al(ob) + 2 * al(yb) + al((size_t)n_vec * 8);
+  rc = grow((unsigned char**)&ws->stage, &ws->stage_cap, need, st);
+  if (rc) return rc;
+  unsigned char* base = (unsigned char*)ws->stage;
+  void* d_ids = base;
+  void* d_w = base + al(ib);
+  int64_t* d_off = (int64_t*)(base + al(ib) + al(wb));
+  double* d_y = (double*)((unsigned char*)d_off + al(ob));
+  u64* d_s = (u64*)((unsigned char*)d_y + al(yb));
+  int64_t* d_em = emitted_out ? (int64_t*)((unsigned char*)d_s + al(yb)) : nullptr;
+  CK(cudaMemcpyAsync(d_ids, ids, ib, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_w, w, wb, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_off, offsets, ob, cudaMemcpyHostToDevice, st));
+  rc = gm_sketch_csr(d_ids, id_bits, d_w, w_bits, d_off, n_vec, k, global_seed, stream_salt,
+                     flags | GM_FLAG_ASYNC, d_y, d_s, d_em, stream);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(y_out, d_y, yb, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(s_out, d_s, yb, cudaMemcpyDeviceToHost, st));
+  if (d_em) CK(cudaMemcpyAsync(emitted_out, d_em, (size_t)n_vec * 8, cudaMemcpyDeviceToHost, st));
+  return check_sync(ws, st);
+}
+
+int gm_sketch_elements(const void* ids, int id_bits, const void* w, int w_bits, int64_t n,
+                       int32_t k, uint64_t global_seed, uint64_t stream_salt, uint32_t flags,
+                       double* y_io, uint64_t* s_io, int64_t* emitted_out, void* stream) {
+  g_msg[0] = 0;
+  int rc = check_common(id_bits, w_bits, k);
+  if (rc) return rc;
+  if (n < 0) return fail(GM_ERR_INVALID_PARAMETER, "n must be >= 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace* ws = nullptr;
+  rc = get_ws(st, &ws);
+  if (rc) return rc;
+  const u64 useed = global_seed, pseed = global_seed ^ stream_salt;
+  const u32 kk = (u32)k;
+  if (id_bits == 32 && w_bits == 32)
+    rc = run_elements<u32, float>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, emitted_out, ws, st);
+  else if (id_bits == 32)
+    rc = run_elements<u32, double>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, emitted_out, ws, st);
+  else if (w_bits == 32)
+    rc = run_elements<u64, float>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, emitted_out, ws, st);
+  else
+    rc = run_elements<u64, double>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, emitted_out, ws, st);
+  if (rc) return rc;
+  const int unset = (int)(ws->host[0] & 0xFFFFFFFFull);
+  if (unset > 0)
+    return fail(GM_ERR_INCOMPLETE, "IncompleteSketchError: %d register(s) unset", unset);
+  return GM_OK;
+}
+
+int gm_sketch_elements_host(const void* ids, int id_bits, const void* w, int w_bits, int64_t n,
+                            int32_t k, uint64_t global_seed, uint64_t stream_salt,
+                            uint32_t flags, double* y_io, uint64_t* s_io, int64_t* emitted_out,
+                            void* stream) {
+  g_msg[0] = 0;
+  int rc = check_common(id_bits, w_bits, k);
+  if (rc) return rc;
+  if (n < 0) return fail(GM_ERR_INVALID_PARAMETER, "n must be >= 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace* ws = nullptr;
+  rc = get_ws(st, &ws);
+  if (rc) return rc;
+  const size_t ib = (size_t)n * (id_bits / 8), wb = (size_t)n * (w_bits / 8), yb = (size_t)k * 8;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  rc = grow((unsigned char**)&ws->stage, &ws->stage_cap, al(ib) + al(wb) + 2 * al(yb), st);
+  if (rc) return rc;
+  unsigned char* base = (unsigned char*)ws->stage;
+  void* d_ids = base;
+  void* d_w = base + al(ib);
+  double* d_y = (double*)(base + al(ib) + al(wb));
+  u64* d_s = (u64*)((unsigned char*)d_y + al(yb));
+  if (n) {
+    CK(cudaMemcpyAsync(d_ids, ids, ib, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_w, w, wb, cudaMemcpyHostToDevice, st));
+  }
+  if (flags & GM_FLAG_ACCUMULATE) {
+    CK(cudaMemcpyAsync(d_y, y_io, yb, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_s, s_io, yb, cudaMemcpyHostToDevice, st));
+  }
+  rc = gm_sketch_elements(d_ids, id_bits, d_w, w_bits, n, k, global_seed, stream_salt, flags, d_y,
+                          d_s, emitted_out, stream);
+  if (rc && rc != GM_ERR_INCOMPLETE) return rc;
+  CK(cudaMemcpyAsync(y_io, d_y, yb, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(s_io, d_s, yb, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return rc;
+}
+
+int gm_merge(const double* y_in, const uint64_t* s_in, int64_t n_sk, int32_t k, double* y_out,
+             uint64_t* s_out, void* stream) {
+  g_msg[0] = 0;
+  if (n_sk < 1) return fail(GM_ERR_MISMATCHED, "MismatchedSketchError: cannot merge an empty list of sketches");
+  if (k < 1) return fail(GM_ERR_INVALID_PARAMETER, "k must be >= 1");
+  const unsigned grid = (unsigned)std::min<int64_t>(((int64_t)k + 255) / 256, 4096);
+  merge_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(y_in, s_in, n_sk, (u32)k, y_out, s_out);
+  CK(cudaGetLastError());
+  return GM_OK;
+}
+
+int gm_match_count(const uint64_t* s_a, const uint64_t* s_b, int64_t n_pairs, int32_t k,
+                   int32_t* matches, void* stream) {
+  g_msg[0] = 0;
+  if (k < 1) return fail(GM_ERR_INVALID_PARAMETER, "k must be >= 1");
+  if (n_pairs <= 0) return GM_OK;
+  match_count_kernel<<<(unsigned)n_pairs, 256, 0, (cudaStream_t)stream>>>(s_a, s_b, n_pairs, (u32)k, matches);
+  CK(cudaGetLastError());
+  return GM_OK;
+}
+
+int gm_uniform_open_batch(const uint64_t* global_seeds, const uint64_t* elements,
+                          const uint64_t* steps, int64_t n, double* out, void* stream) {
+  g_msg[0] = 0;
+  if (n <= 0) return GM_OK;
+  uniform_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(global_seeds, elements, steps, n, out);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return GM_OK;
+}
+
+int gm_perm_draw_batch(const uint64_t* perm_seeds, const uint64_t* elements, const uint64_t* steps,
+                       const uint32_t* ks, int64_t n, uint32_t* out, void* stream) {
+  g_msg[0] = 0;
+  if (n <= 0) return GM_OK;
+  randint_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(perm_seeds, elements, steps, ks, n, out);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return GM_OK;
+}
+
+int gm_probe_arrival_rate(int64_t n_threads, int32_t iters, int32_t k, double* sink, void* stream) {
+  g_msg[0] = 0;
+  if (k < 2 || k > 65536 || iters < 1 || n_threads < NT)
+    return fail(GM_ERR_INVALID_PARAMETER, "bad probe arguments");
+  arrival_probe_kernel<<<(unsigned)(n_threads / NT), NT, 0, (cudaStream_t)stream>>>(
+      iters, (u32)k, 0x1234ull, 0x5678ull, sink);
+  CK(cudaGetLastError());
+  return GM_OK;
+}
+
+int gm_count_arrivals_csr(const void* ids, int id_bits, const void* w, int w_bits,
+                          const int64_t* offsets, int64_t n_vec, int32_t k, uint64_t global_seed,
+                          const double* tau, unsigned long long* counts, void* stream) {
+  g_msg[0] = 0;
+  int rc = check_common(id_bits, w_bits, k);
+  if (rc) return rc;
+  if (n_vec <= 0) return GM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(counts, 0, (size_t)n_vec * 8, st));
+  const unsigned g = (unsigned)n_vec;
+  if (id_bits == 32 && w_bits == 32)
+    count_le_kernel<u32, float><<<g, NT, 0, st>>>((const u32*)ids, (const float*)w, offsets, n_vec, (u32)k, global_seed, tau, counts);
+  else if (id_bits == 32)
+    count_le_kernel<u32, double><<<g, NT, 0, st>>>((const u32*)ids, (const double*)w, offsets, n_vec, (u32)k, global_seed, tau, counts);
+  else if (w_bits == 32)
+    count_le_kernel<u64, float><<<g, NT, 0, st>>>((const u64*)ids, (const float*)w, offsets, n_vec, (u32)k, global_seed, tau, counts);
+  else
+    count_le_kernel<u64, double><<<g, NT, 0, st>>>((const u64*)ids, (const double*)w, offsets, n_vec, (u32)k, global_seed, tau, counts);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  return GM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,458 @@
+// gm_kernels.cuh -- the FastGM kernels (sm_100a).
+//
+//   K1 csr_sketch_kernel   batch of CSR vectors, persistent CTAs, one vector
+//                          per CTA at a time, registers in shared memory
+//                          (configs 1-3; replaces sketch_fast_counted,
+//                          sketch.py:218-311, per vector).
+//   K2 elem_light_kernel + elem_heavy_kernel
+//                          one huge element set (a huge vector or an
+//                          (id, weight) stream), grid-stride, registers in
+//                          global memory (configs 4-5; replaces
+//                          sketch_stream / stream_update, stream.py:58-153).
+//   K4 merge_kernel        per-register min over sketches, earlier sketch
+//                          wins ties (estimate.py:103-125).
+//   estimator kernels      register-match counts (estimate.py:47-55).
+#pragma once
+
+#include "gm_walk.cuh"
+
+namespace gmk {
+
+constexpr int NT = 256;           // threads per CTA
+constexpr int NWARP = NT / 32;
+constexpr int LIGHT_CAP = 32;     // light-walker list entries per thread
+constexpr int HEAVY_LIST = 512;   // per-CTA heavy-element list
+constexpr u32 DENSE_SMEM_MAX_K = 2048;
+
+// device-side error word: code in the low 32 bits (gm error enum), the
+// first offending vector/element index in the high 32 bits
+__device__ __forceinline__ void raise_error(unsigned long long* err, u32 code, u64 where) {
+  atomicCAS(err, 0ull, ((unsigned long long)(where & 0xFFFFFFFFull) << 32) | code);
+}
+
+template <class T>
+__device__ __forceinline__ double load_w(const T* w, int64_t i) {
+  return (double)__ldg(&w[i]);
+}
+template <class T>
+__device__ __forceinline__ u64 load_id(const T* ids, int64_t i) {
+  return (u64)__ldg(&ids[i]);
+}
+
+__device__ __forceinline__ bool weight_ok(double w) {
+  // WeightedVector / stream_update validation (sketch.py:57-64, stream.py:63-66)
+  return isfinite(w) && w > 0.0 && w >= 1e-300;
+}
+
+// threshold for pass `attempt` given total weight W (tau
+// bounds the final max register with probability 1 - e^-c)
+__device__ __forceinline__ double pass_tau(double W, u32 k, int attempt) {
+  const double c = attempt == 0 ? 2.5 : attempt == 1 ? 6.0 : attempt == 2 ? 14.0 : -1.0;
+  if (c < 0.0) return __longlong_as_double(0x7FF0000000000000ll);  // +inf: full queues
+  return (log((double)k) + c) / W;
+}
+
+struct CsrSmem {
+  int unset;
+  int next_light;
+  int n_heavy;
+  int heavy_overflow;
+  int vec;
+  u32 stamp;
+  unsigned long long emitted;
+  double wsum[NWARP];
+};
+
+// K1.  Dynamic shared memory layout:
+//   Reg regs[k] | union{ u32 light[LIGHT_CAP][NT], u32 dense[NWARP][k] (k <= DENSE_SMEM_MAX_K) }
+//   | double scan[NWARP][32] | int prov[NWARP][32] | u32 heavy[HEAVY_LIST]
+template <class IdT, class WT>
+__global__ void __launch_bounds__(NT, 3)
+    csr_sketch_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts,
+                      const int64_t* __restrict__ offsets, int64_t n_vec, u32 k, u64 useed,
+                      u64 pseed, double* __restrict__ y_out, u64* __restrict__ s_out,
+                      int64_t* __restrict__ emitted_out, int* __restrict__ vec_counter,
+                      u32* __restrict__ dense_global, unsigned long long* __restrict__ err,
+                      int attempt0) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ CsrSmem S;
+  Reg* regs = reinterpret_cast<Reg*>(smem_raw);
+  u32* pool = reinterpret_cast<u32*>(smem_raw + (size_t)k * sizeof(Reg));
+  const bool dense_in_smem = k <= DENSE_SMEM_MAX_K;
+  const size_t pool_words = dense_in_smem ? max((size_t)LIGHT_CAP * NT, (size_t)NWARP * k)
+                                          : (size_t)LIGHT_CAP * NT;
+  double* scan_all = reinterpret_cast<double*>(pool + pool_words);
+  int* prov_all = reinterpret_cast<int*>(scan_all + NWARP * 32);
+  u32* heavy = reinterpret_cast<u32*>(prov_all + NWARP * 32);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  u32* dense = dense_in_smem ? pool + (size_t)warp * k
+                             : dense_global + ((size_t)blockIdx.x * NWARP + warp) * k;
+  if (tid == 0) S.stamp = 0;
+  // dense stamps start clean
+  if (dense_in_smem) {
+    // (re-initialised lazily below when the stamp wraps)
+  } else {
+    for (u32 i = lane; i < k; i += 32) dense[i] = 0;
+  }
+  __syncthreads();
+
+  for (;;) {
+    if (tid == 0) S.vec = atomicAdd(vec_counter, 1);
+    __syncthreads();
+    const int64_t v = S.vec;
+    if (v >= n_vec) break;
+    const int64_t lo = offsets[v], hi = offsets[v + 1];
+    const int n = (int)(hi - lo);
+
+    // total weight (only sets tau) + validation
+    double ws = 0.0;
+    for (int i = tid; i < n; i += NT) {
+      const double w = load_w(wts, lo + i);
+      if (!weight_ok(w)) raise_error(err, 2u, (u64)v);
+      ws += w;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ws += __shfl_xor_sync(0xFFFFFFFFu, ws, o);
+    if (lane == 0) S.wsum[warp] = ws;
+    for (u32 j = tid; j < k; j += NT) {
+      regs[j].y = INF_BITS;
+      regs[j].id = NO_ID;
+    }
+    if (tid == 0) {
+      S.unset = (int)k;
+      S.emitted = 0;
+    }
+    __syncthreads();
+    double W = 0.0;
+#pragma unroll
+    for (int i = 0; i < NWARP; ++i) W += S.wsum[i];
+    if (n == 0) {
+      if (tid == 0) raise_error(err, 1u, (u64)v);
+    }
+
+    u32 emitted = 0;
+    for (int attempt = attempt0; n > 0; ++attempt) {
+      const double tau = pass_tau(W, k, attempt);
+      const double light_w = 8.0 / ((double)k * tau);  // expected depth k*w*tau < 8
+      if (tid == 0) {
+        S.next_light = 0;
+        S.n_heavy = 0;
+        S.heavy_overflow = 0;
+      }
+      __syncthreads();
+      // ---- light phase: one thread per element, dynamic grab
+      u32* mymap = pool + tid;
+      for (;;) {
+        const int i = atomicAdd(&S.next_light, 1);
+        if (i >= n) break;
+        const double w = load_w(wts, lo + i);
+        bool ok = false;
+        if (w < light_w) {
+          ok = walk_light<true>(load_id(ids, lo + i), w, tau, k, useed, pseed, mymap, NT,
+                                LIGHT_CAP, regs, &S.unset, emitted);
+        }
+        if (!ok) {
+          const int h = atomicAdd(&S.n_heavy, 1);
+          if (h < HEAVY_LIST)
+            heavy[h] = (u32)i;
+          else
+            S.heavy_overflow = 1;
+        }
+      }
+      __syncthreads();
+      // ---- heavy phase: one warp per element
+      const bool all = S.heavy_overflow != 0;
+      const int nh = all ? n : min(S.n_heavy, HEAVY_LIST);
+      if (dense_in_smem) {
+        for (u32 i = tid; i < (u32)NWARP * k; i += NT) pool[i] = 0;
+        __syncthreads();
+      }
+      if (tid == 0) S.next_light = 0;
+      __syncthreads();
+      u32 stamp = 0;
+      double* scan = scan_all + warp * 32;
+      int* prov = prov_all + warp * 32;
+      for (;;) {
+        int hidx = 0;
+        if (lane == 0) hidx = atomicAdd(&S.next_light, 1);
+        hidx = __shfl_sync(0xFFFFFFFFu, hidx, 0);
+        if (hidx >= nh) break;
+        const int i = all ? hidx : (int)heavy[hidx];
+        if (++stamp == 0x10000u) {  // stamp wrap: clear this warp's array
+          for (u32 q = lane; q < k; q += 32) dense[q] = 0;
+          __syncwarp();
+          stamp = 1;
+        }
+        u32 em = 0;
+        walk_warp<true>(load_id(ids, lo + i), load_w(wts, lo + i), tau, k, useed, pseed, dense,
+                        stamp, scan, prov, regs, &S.unset, em);
+        if (lane == 0) emitted += em;
+      }
+      if (!dense_in_smem) {
+        // global dense arrays must not carry stamps into the next pass
+        __syncwarp();
+        for (u32 q = lane; q < k; q += 32) dense[q] = 0;
+      }
+      __syncthreads();
+      if (S.unset == 0) break;
+      __syncthreads();
+    }
+
+    // emitted count + outputs
+    if (emitted_out) {
+      unsigned long long e = emitted;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xFFFFFFFFu, e, o);
+      if (lane == 0) atomicAdd(&S.emitted, e);
+    }
+    __syncthreads();
+    for (u32 j = tid; j < k; j += NT) {
+      y_out[v * (int64_t)k + j] = __longlong_as_double((long long)regs[j].y);
+      s_out[v * (int64_t)k + j] = regs[j].id;
+    }
+    if (tid == 0 && emitted_out) emitted_out[v] = (int64_t)S.emitted;
+    __syncthreads();
+  }
+}
+
+// ---- K2: one huge element set, registers in global memory ---------------
+// light pass: grid-stride, one thread per element; heavy/overflowing
+// elements are appended to heavy_list and walked by elem_heavy_kernel.
+template <class IdT, class WT>
+__global__ void __launch_bounds__(NT)
+    elem_light_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, int64_t n, u32 k,
+                      u64 useed, u64 pseed, const double* __restrict__ tau_p, Reg* regs,
+                      int* unset_ctr, u64* __restrict__ heavy_list, int64_t heavy_cap,
+                      unsigned long long* heavy_count, unsigned long long* emitted_total,
+                      unsigned long long* __restrict__ err) {
+  __shared__ u32 maps[16 * NT];
+  const double tau = *tau_p;
+  const double light_w = 8.0 / ((double)k * tau);
+  u32 emitted = 0;
+  u32* mymap = maps + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * NT;
+  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += stride) {
+    const double w = load_w(wts, i);
+    if (!weight_ok(w)) {
+      raise_error(err, 2u, (u64)i);
+      continue;
+    }
+    bool ok = false;
+    if (w < light_w)
+      ok = walk_light<false>(load_id(ids, i), w, tau, k, useed, pseed, mymap, NT, 16, regs,
+                             unset_ctr, emitted);
+    if (!ok) {
+      const unsigned long long h = atomicAdd(heavy_count, 1ull);
+      if ((int64_t)h < heavy_cap) heavy_list[h] = (u64)i;
+    }
+  }
+  if (emitted_total) {
+    unsigned long long e = emitted;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xFFFFFFFFu, e, o);
+    if ((threadIdx.x & 31) == 0 && e) atomicAdd(emitted_total, e);
+  }
+}
+
+// one warp per heavy element; dense arrays in global scratch, one per warp
+template <class IdT, class WT>
+__global__ void __launch_bounds__(NT)
+    elem_heavy_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, u32 k, u64 useed,
+                      u64 pseed, const double* __restrict__ tau_p, Reg* regs, int* unset_ctr,
+                      const u64* __restrict__ heavy_list, const unsigned long long* heavy_count,
+                      int64_t heavy_cap, u32* __restrict__ dense_global,
+                      unsigned long long* emitted_total) {
+  __shared__ double scan_all[NWARP * 32];
+  __shared__ int prov_all[NWARP * 32];
+  const double tau = *tau_p;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nh = min((int64_t)*heavy_count, heavy_cap);
+  const int64_t gw = (int64_t)blockIdx.x * NWARP + warp;
+  u32* dense = dense_global + (size_t)gw * k;
+  u32 stamp = 0, emitted = 0;
+  for (int64_t h = gw; h < nh; h += (int64_t)gridDim.x * NWARP) {
+    const int64_t i = (int64_t)heavy_list[h];
+    if (++stamp == 0x10000u) {
+      for (u32 q = lane; q < k; q += 32) dense[q] = 0;
+      __syncwarp();
+      stamp = 1;
+    }
+    u32 em = 0;
+    walk_warp<false>(load_id(ids, i), load_w(wts, i), tau, k, useed, pseed, dense, stamp,
+                     scan_all + warp * 32, prov_all + warp * 32, regs, unset_ctr, em);
+    if (lane == 0) emitted += em;
+  }
+  // leave the scratch clean for the next launch
+  __syncwarp();
+  if (stamp)
+    for (u32 q = lane; q < k; q += 32) dense[q] = 0;
+  if (emitted_total && lane == 0 && emitted) atomicAdd(emitted_total, (unsigned long long)emitted);
+}
+
+__global__ void init_regs_kernel(Reg* regs, u32 k, int* unset_ctr) {
+  for (u32 j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    regs[j].y = INF_BITS;
+    regs[j].id = NO_ID;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *unset_ctr = (int)k;
+}
+
+// registers from caller-provided (y, s) (accumulate mode); counts unset ones
+__global__ void load_regs_kernel(Reg* regs, u32 k, const double* y, const u64* s, int* unset_ctr) {
+  for (u32 j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    const u64 yb = (u64)__double_as_longlong(y[j]);
+    regs[j].y = yb;
+    regs[j].id = s[j];
+    if (yb == INF_BITS) atomicAdd(unset_ctr, 1);
+  }
+}
+
+__global__ void store_regs_kernel(const Reg* regs, u32 k, double* y, u64* s) {
+  for (u32 j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    y[j] = __longlong_as_double((long long)regs[j].y);
+    s[j] = regs[j].id;
+  }
+}
+
+// tau from the total weight, or from the unset fraction f of the previous
+// pass (P(register unset) = exp(-W tau) => W ~ -ln f / tau).
+__global__ void tau_kernel(double* tau, const double* wsum, u32 k, int attempt, const int* unset_ctr) {
+  if (threadIdx.x || blockIdx.x) return;
+  const double lk = log((double)k);
+  if (attempt == 0) {
+    *tau = (lk + 3.0) / *wsum;
+    return;
+  }
+  const double prev = *tau;
+  const int unset = *unset_ctr;
+  const double f = (double)unset / (double)k;
+  double W_est = f < 1.0 ? -log(f) / prev : 0.0;
+  double next;
+  if (attempt >= 5)
+    next = __longlong_as_double(0x7FF0000000000000ll);
+  else if (W_est > 0.0)
+    next = fmax((lk + 3.0 + 2.0 * attempt) / W_est, 2.0 * prev);
+  else
+    next = prev * (double)k;
+  *tau = next;
+}
+
+// weight sum (for the first tau) over a strided sample, scaled to n
+template <class WT>
+__global__ void weight_sample_kernel(const WT* __restrict__ wts, int64_t n, int64_t step,
+                                     double* out) {
+  double s = 0.0;
+  int64_t cnt = 0;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * step; i < n;
+       i += (int64_t)gridDim.x * blockDim.x * step) {
+    const double w = (double)wts[i];
+    if (isfinite(w) && w > 0.0) s += w;
+    ++cnt;
+  }
+  s *= (double)step;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
+// ---- K4 merge ----
+__global__ void merge_kernel(const double* __restrict__ y_in, const u64* __restrict__ s_in,
+                             int64_t n_sk, u32 k, double* __restrict__ y_out,
+                             u64* __restrict__ s_out) {
+  for (u32 j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    double y = y_in[j];
+    u64 s = s_in[j];
+    for (int64_t r = 1; r < n_sk; ++r) {
+      const double t = y_in[r * k + j];
+      if (t < y) {  // strict: earlier sketch wins ties (estimate.py:121-124)
+        y = t;
+        s = s_in[r * k + j];
+      }
+    }
+    y_out[j] = y;
+    s_out[j] = s;
+  }
+}
+
+// ---- estimators: register matches of sketch pairs (estimate.py:54) ----
+__global__ void match_count_kernel(const u64* __restrict__ s_a, const u64* __restrict__ s_b,
+                                   int64_t n_pairs, u32 k, int32_t* __restrict__ matches) {
+  const int64_t p = blockIdx.x;
+  if (p >= n_pairs) return;
+  int c = 0;
+  for (u32 j = threadIdx.x; j < k; j += blockDim.x) c += s_a[p * k + j] == s_b[p * k + j];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  __shared__ int part[32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += part[i];
+    matches[p] = t;
+  }
+}
+
+// ---- K0 test kernels: the keyed streams element by element ----
+__global__ void uniform_kernel(const u64* seeds, const u64* elems, const u64* steps, int64_t n,
+                               double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = u_open(mix64(seeds[i] + elems[i] * K_ELEM + steps[i] * K_STEP));
+}
+
+__global__ void randint_kernel(const u64* pseeds, const u64* elems, const u64* steps,
+                               const u32* ks, int64_t n, u32* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = perm_draw(pseeds[i] + elems[i] * K_ELEM, (u32)steps[i], ks[i]);
+}
+
+// ---- diagnostics ----
+// Speed-of-light probe for the arrival generator: every thread emits a
+// long run of exact arrivals (spacing + permutation draw) with no pruning,
+// no registers, no divergence and no memory traffic.  Its rate is the
+// compute roofline the sketch kernels are reported against.
+__global__ void __launch_bounds__(NT) arrival_probe_kernel(int iters, u32 k, u64 useed, u64 pseed,
+                                                           double* sink) {
+  const u64 id = (u64)blockIdx.x * NT + threadIdx.x;
+  const u64 ubase = useed + id * K_ELEM, pbase = pseed + id * K_ELEM;
+  double b = 0.0;
+  u32 acc = 0;
+  const double w = 1.0 + (double)(threadIdx.x & 7);
+  for (int i = 0; i < iters; ++i) {
+    const u32 z = 1u + ((u32)i % (k - 1u));
+    b = __dadd_rn(b, spacing(ubase, z, w, k));
+    acc += perm_draw(pbase, z, k);
+  }
+  if (b == -1.0 || acc == 0xFFFFFFFFu) sink[0] = b + (double)acc;
+}
+
+// Number of arrivals t <= tau_v of every element of every CSR vector
+// (times only; the algorithmic survivor count of a pass at tau_v).
+template <class IdT, class WT>
+__global__ void __launch_bounds__(NT) count_le_kernel(const IdT* __restrict__ ids,
+                                                      const WT* __restrict__ wts,
+                                                      const int64_t* __restrict__ offsets,
+                                                      int64_t n_vec, u32 k, u64 useed,
+                                                      const double* __restrict__ tau,
+                                                      unsigned long long* __restrict__ counts) {
+  const int64_t v = blockIdx.x;
+  if (v >= n_vec) return;
+  const double t_v = tau[v];
+  unsigned long long c = 0;
+  for (int64_t i = offsets[v] + threadIdx.x; i < offsets[v + 1]; i += NT) {
+    const u64 ubase = useed + load_id(ids, i) * K_ELEM;
+    const double w = load_w(wts, i);
+    double b = 0.0;
+    for (u32 z = 1; z <= k; ++z) {
+      b = __dadd_rn(b, spacing(ubase, z, w, k));
+      if (b > t_v) break;
+      ++c;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&counts[v], c);
+}
+
+}  // namespace gmk

@@ -1,0 +1,172 @@
+// gm_walk.cuh -- element-queue walkers (the device form of _run_queue,
+// randgen.py:158-207, driven to a threshold instead of a fixed cursor).
+//
+// A walker emits an element's arrivals in ascending order and folds every
+// arrival t <= tau into the registers; it stops at the first arrival > tau
+// (that arrival and all later ones exceed tau).  When every register is set
+// at the end of a pass, tau bounds the final maximum register, so every
+// arrival that can win a register was emitted and the sketch equals
+// sketch_naive's (the schedule-independence sketch_fast relies on,
+// sketch.py:277-282).  Re-emitting an arrival is a no-op on the registers,
+// so a pass can be repeated with a larger tau without undoing anything.
+//
+// The Fisher-Yates state (LazyPermutation, randgen.py:146-155) is sparse:
+//  * light walker (one thread per element): a linear list of
+//    (position, value) pairs in the thread's shared-memory slice; the entry
+//    at position z-1 dies at step z, so the list holds only positions >= z.
+//  * warp walker (32 steps of one element per iteration): a stamped dense
+//    array of k words; the 32 swaps of a batch are resolved in parallel by
+//    provider chains (see walk_warp).
+#pragma once
+
+#include "gm_core.cuh"
+
+namespace gmk {
+
+struct WalkStats {
+  u32 emitted;  // arrivals computed (accepted + the terminating one)
+};
+
+// ---- light walker -------------------------------------------------------
+// map: this thread's slice, entry e at map[e * stride]; entries are
+// (pos << 16) | (val - 1).  Returns false if the list overflowed (the caller
+// re-walks the element with the warp walker; registers already updated
+// stay valid).
+template <bool kSharedRegs>
+__device__ __forceinline__ bool walk_light(u64 id, double w, double tau, u32 k, u64 useed,
+                                           u64 pseed, u32* map, int stride, int cap, Reg* regs,
+                                           int* unset_ctr, u32& emitted) {
+  const u64 ubase = useed + id * K_ELEM;
+  const u64 pbase = pseed + id * K_ELEM;
+  double b = 0.0;
+  int nl = 0;
+  u32 z = 0;
+  while (z < k) {
+    ++z;
+    const double t = __dadd_rn(b, spacing(ubase, z, w, k));
+    if (t > tau) break;
+    b = t;
+    const u32 j = perm_draw(pbase, z, k);
+    const u32 zi = z - 1, ji = j - 1;
+    u32 vz = zi + 1, vj = ji + 1;
+    int sz = -1, sj = -1;
+    for (int e = 0; e < nl; ++e) {
+      const u32 ent = map[e * stride];
+      const u32 p = ent >> 16;
+      if (p == zi) {
+        vz = (ent & 0xFFFFu) + 1;
+        sz = e;
+      }
+      if (p == ji) {
+        vj = (ent & 0xFFFFu) + 1;
+        sj = e;
+      }
+    }
+    // perm[zi] <- vj (dead from now on), perm[ji] <- vz
+    if (ji != zi) {
+      const u32 nent = (ji << 16) | (vz - 1);
+      if (sj >= 0) {
+        map[sj * stride] = nent;
+        if (sz >= 0) {  // drop the dead zi entry
+          --nl;
+          if (sz != nl) map[sz * stride] = map[nl * stride];
+        }
+      } else if (sz >= 0) {
+        map[sz * stride] = nent;  // reuse the dead slot
+      } else {
+        if (nl == cap) {
+          emitted += z;
+          return false;
+        }
+        map[nl * stride] = nent;
+        ++nl;
+      }
+    } else if (sz >= 0) {
+      --nl;
+      if (sz != nl) map[sz * stride] = map[nl * stride];
+    }
+    if (reg_min<kSharedRegs>(&regs[vj - 1], (u64)__double_as_longlong(t), id))
+      atomicSub(unset_ctr, 1);
+  }
+  emitted += z;
+  return true;
+}
+
+// ---- warp walker ----------------------------------------------------------
+// dense: k words, entry (stamp << 16) | (val - 1); other stamps read as the
+// identity.  scan: 32 doubles, prov: 32 ints (per-warp shared scratch).
+__device__ __forceinline__ u32 dget(const u32* dense, u32 pos, u32 stamp) {
+  const u32 e = dense[pos];
+  return (e >> 16) == stamp ? (e & 0xFFFFu) + 1 : pos + 1;
+}
+
+template <bool kSharedRegs>
+__device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u64 useed,
+                                          u64 pseed, u32* dense, u32 stamp, double* scan,
+                                          int* prov, Reg* regs, int* unset_ctr, u32& emitted) {
+  const unsigned FULL = 0xFFFFFFFFu;
+  const int lane = threadIdx.x & 31;
+  const u64 ubase = useed + id * K_ELEM;
+  const u64 pbase = pseed + id * K_ELEM;
+  double b = 0.0;
+  u32 z0 = 0;
+  while (z0 < k) {
+    const u32 z = z0 + lane + 1;
+    const bool valid = z <= k;
+    const double d = valid ? spacing(ubase, z, w, k) : 0.0;
+    scan[lane] = d;
+    prov[lane] = -1;
+    __syncwarp();
+    if (lane == 0) {  // left-to-right prefix, the reference's summation order
+      double acc = b;
+#pragma unroll 8
+      for (int i = 0; i < 32; ++i) {
+        acc = __dadd_rn(acc, scan[i]);
+        scan[i] = acc;
+      }
+    }
+    __syncwarp();
+    const double t = scan[lane];
+    const u32 stop = __ballot_sync(FULL, !(valid && t <= tau));
+    const int n_acc = stop ? __ffs(stop) - 1 : 32;
+    const bool acc = lane < n_acc;
+    const u32 j = acc ? perm_draw(pbase, z, k) : 0u;
+    const u32 zi = z - 1, ji = j - 1;
+    u32 vz = acc ? dget(dense, zi, stamp) : 0u;
+    const u32 mj = acc ? dget(dense, ji, stamp) : 0u;
+    // provider of position zi: last earlier lane whose ji == zi
+    const int tgt = (int)ji - (int)z0;
+    if (acc && tgt > lane && tgt < n_acc) atomicMax(&prov[tgt], lane);
+    __syncwarp();
+    int p = acc ? prov[lane] : -1;
+    // provider of position ji: last earlier lane with the same ji
+    const u32 same = __match_any_sync(FULL, acc ? ji : (0x80000000u | (u32)lane));
+    const u32 lower = same & ((1u << lane) - 1u);
+    const int pj = lower ? 31 - __clz(lower) : -1;
+    // resolve vz through provider chains (pointer jumping)
+    while (__any_sync(FULL, p >= 0)) {
+      const int src = p >= 0 ? p : lane;
+      const u32 v2 = __shfl_sync(FULL, vz, src);
+      const int p2 = __shfl_sync(FULL, p, src);
+      if (p >= 0) {
+        vz = v2;
+        p = p2;
+      }
+    }
+    const u32 vjp = __shfl_sync(FULL, vz, pj >= 0 ? pj : lane);
+    const u32 vj = pj >= 0 ? vjp : mj;
+    // positions >= z0 + n_acc stay live: last writer of each ji stores vz
+    const u32 higher = same & ~((2u << lane) - 1u);
+    if (acc && higher == 0 && ji >= z0 + (u32)n_acc) dense[ji] = (stamp << 16) | (vz - 1);
+    if (acc && reg_min<kSharedRegs>(&regs[vj - 1], (u64)__double_as_longlong(t), id))
+      atomicSub(unset_ctr, 1);
+    emitted += (u32)(n_acc + (n_acc < 32 && z0 + n_acc < k ? 1 : 0));
+    if (n_acc < 32) break;
+    b = __shfl_sync(FULL, t, 31);
+    z0 += 32;
+    __syncwarp();
+  }
+  __syncwarp();
+}
+
+}  // namespace gmk

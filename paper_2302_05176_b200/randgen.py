@@ -1,0 +1,126 @@
+"""Seed schemes and the keyed random streams (reference randgen.py).
+
+SeedScheme / derive_seed / mix64 are the reference's 64-bit key algebra
+(randgen.py:64-104) on two host integers.  The streams themselves
+(uniform_open, the permutation draw) are evaluated by the CUDA library:
+uniform_open_batch and perm_draw_batch run the device K0 functions that
+every sketch kernel uses, so tests can pin them bit-for-bit against the
+reference.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device
+
+MASK64 = (1 << 64) - 1
+
+# randgen.py:46-61 (must never change: every sketch depends on them)
+K_ELEM = 0x9E3779B97F4A7C15
+K_STEP = 0xC2B2AE3D27D4EB4F
+K_RETRY = 0xD6E8FEB86659FD93
+_M1 = 0xBF58476D1CE4E5B9
+_M2 = 0x94D049BB133111EB
+DEFAULT_STREAM_SALT = 0x6A09E667F3BCC909
+MIN_WEIGHT = 1e-300
+
+
+def mix64(x: int) -> int:
+    """splitmix64 finalizer (randgen.py:64-69)."""
+    x &= MASK64
+    x = ((x ^ (x >> 30)) * _M1) & MASK64
+    x = ((x ^ (x >> 27)) * _M2) & MASK64
+    return x ^ (x >> 31)
+
+
+@dataclass(frozen=True)
+class SeedScheme:
+    """(global_seed, stream_salt), both masked to 64 bits (randgen.py:72-95)."""
+
+    global_seed: int
+    stream_salt: int = DEFAULT_STREAM_SALT
+
+    def __post_init__(self):
+        object.__setattr__(self, "global_seed", self.global_seed & MASK64)
+        object.__setattr__(self, "stream_salt", self.stream_salt & MASK64)
+
+    @property
+    def perm_seed(self) -> int:
+        return self.global_seed ^ self.stream_salt
+
+    @property
+    def fingerprint(self) -> int:
+        return mix64(self.global_seed + mix64(self.stream_salt))
+
+
+def derive_seed(master: int, index: int) -> int:
+    """Child seed for trial ``index`` (randgen.py:98-104)."""
+    return mix64((master + (index + 1) * K_ELEM) & MASK64)
+
+
+class LazyPermutation(dict):
+    """Sparse Fisher-Yates array of 1..k (randgen.py:146-155)."""
+
+    def __missing__(self, index):
+        return index + 1
+
+
+def _u64_tensor(values, dev) -> torch.Tensor:
+    a = np.asarray([int(v) & MASK64 for v in values], dtype=np.uint64) if not isinstance(
+        values, np.ndarray) else np.ascontiguousarray(values.astype(np.uint64))
+    return torch.from_numpy(a.view(np.int64)).to(dev)
+
+
+def uniform_open_batch(seeds, elements, steps) -> np.ndarray:
+    """uniform_open (randgen.py:107-119) for arrays of (seed, element, step),
+    evaluated on the device by the K0 stream the kernels use."""
+    dev = _device.require_cuda()
+    s = _u64_tensor(seeds, dev)
+    e = _u64_tensor(elements, dev)
+    z = _u64_tensor(steps, dev)
+    n = s.numel()
+    if np.any(np.asarray(steps, dtype=np.int64) < 1):
+        raise ValueError("step must be >= 1")
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    _device.call("gm_uniform_open_batch", s.data_ptr(), e.data_ptr(), z.data_ptr(), n,
+                 out.data_ptr(), _device.stream_ptr())
+    return out.cpu().numpy()
+
+
+def uniform_open(scheme: SeedScheme, element: int, step: int) -> float:
+    if step < 1:
+        raise ValueError(f"step must be >= 1, got {step}")
+    return float(uniform_open_batch([scheme.global_seed], [element], [step])[0])
+
+
+def perm_draw_batch(perm_seeds, elements, steps, ks) -> np.ndarray:
+    """j in [z, k] = rand_int_between(scheme, e, z, z, k) (randgen.py:122-143)
+    on the device, for k - z + 1 <= 65536."""
+    dev = _device.require_cuda()
+    p = _u64_tensor(perm_seeds, dev)
+    e = _u64_tensor(elements, dev)
+    z = _u64_tensor(steps, dev)
+    kk = torch.as_tensor(np.asarray(ks, dtype=np.int64).astype(np.int32), device=dev)
+    n = p.numel()
+    out = torch.empty(n, dtype=torch.int32, device=dev)
+    _device.call("gm_perm_draw_batch", p.data_ptr(), e.data_ptr(), z.data_ptr(), kk.data_ptr(), n,
+                 out.data_ptr(), _device.stream_ptr())
+    return out.cpu().numpy().astype(np.int64)
+
+
+def rand_int_between(scheme: SeedScheme, element: int, step: int, lo: int, hi: int) -> int:
+    """Unbiased integer in [lo, hi] (randgen.py:122-143), hi - lo < 65536."""
+    if step < 1:
+        raise ValueError(f"step must be >= 1, got {step}")
+    if hi < lo:
+        raise ValueError(f"empty range [{lo}, {hi}]")
+    m = hi - lo + 1
+    if m > 65536:
+        raise ValueError("ranges wider than 65536 are outside the device draw")
+    # the device draw is z + (g mod m) with m = k - z + 1; key is (element, step)
+    j = perm_draw_batch([scheme.perm_seed], [element], [step], [step + m - 1])[0]
+    return lo + int(j) - step

@@ -1,0 +1,345 @@
+"""Sketch types and generators (reference sketch.py), backed by the CUDA
+engine.
+
+Types keep the reference's names, fields and validation (WeightedVector
+sketch.py:40-115, GumbelMaxSketch :118-136, GenerationParams :139-157).
+Generators run on the device:
+  sketch_fast / sketch_fast_counted   -> gm_sketch_csr (K1), or
+                                         gm_sketch_elements (K2) for vectors
+                                         above LARGE_VECTOR elements
+  sketch_naive / sketch_naive_counted -> the same kernels with every queue
+                                         run to k (GM_FLAG_EXHAUSTIVE)
+  sketch_csr / sketch_many            -> batched K1 over CSR arrays (new; the
+                                         reference callers loop per vector)
+Registers equal the reference's: s bit-exact; y within the documented
+tolerance (the device log is CUDA's, not glibc's).
+The *_counted work counters count arrivals the device computed, which is
+schedule-dependent and differs from the reference's FastSearch count.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass
+from typing import Iterator, Mapping, Sequence
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from .errors import (
+    EmptyVectorError,
+    InvalidParameterError,
+    InvalidWeightError,
+    MismatchedSketchError,
+    MissingElementError,
+)
+from .randgen import MIN_WEIGHT, SeedScheme
+
+SKETCH_FORMAT = "gmsketch/1"
+LARGE_VECTOR = 1 << 20  # above this a single vector uses the grid-wide kernel
+UINT64_MAX = (1 << 64) - 1
+
+
+class WeightedVector:
+    """Sparse map element index (>= 1) -> weight > 0 (sketch.py:40-115)."""
+
+    __slots__ = ("_items", "_index", "_weight_sum", "_ids", "_w")
+
+    def __init__(self, entries: Mapping[int, float]):
+        items = []
+        for element, weight in entries.items():
+            element = int(element)
+            if element < 1:
+                raise InvalidWeightError(f"element indices must be >= 1, got {element}")
+            weight = float(weight)
+            if not math.isfinite(weight) or weight <= 0.0:
+                raise InvalidWeightError(
+                    f"element {element}: weight must be positive and finite, got {weight}")
+            if weight < MIN_WEIGHT:
+                raise InvalidWeightError(
+                    f"element {element}: weight {weight} below minimum {MIN_WEIGHT}")
+            items.append((element, weight))
+        items.sort()
+        self._items = tuple(items)
+        self._index = dict(items)
+        self._weight_sum = math.fsum(w for _, w in items)
+        self._ids = None
+        self._w = None
+
+    @classmethod
+    def from_arrays(cls, ids, weights) -> "WeightedVector":
+        return cls(dict(zip((int(e) for e in ids), (float(w) for w in weights))))
+
+    @property
+    def n_plus(self) -> int:
+        return len(self._items)
+
+    @property
+    def weight_sum(self) -> float:
+        return self._weight_sum
+
+    def items(self):
+        return self._items
+
+    def arrays(self) -> tuple[np.ndarray, np.ndarray]:
+        """(ids uint64, weights float64) in ascending id order."""
+        if self._ids is None:
+            self._ids = np.array([e for e, _ in self._items], dtype=np.uint64)
+            self._w = np.array([w for _, w in self._items], dtype=np.float64)
+        return self._ids, self._w
+
+    def get(self, element: int, default: float = 0.0) -> float:
+        return self._index.get(element, default)
+
+    def __getitem__(self, element: int) -> float:
+        try:
+            return self._index[element]
+        except KeyError:
+            raise MissingElementError(f"element {element} not in vector") from None
+
+    def __contains__(self, element: int) -> bool:
+        return element in self._index
+
+    def __len__(self) -> int:
+        return len(self._items)
+
+    def __iter__(self) -> Iterator[int]:
+        return iter(self._index)
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, WeightedVector):
+            return NotImplemented
+        return self._items == other._items
+
+    def __repr__(self) -> str:
+        return f"WeightedVector(n_plus={self.n_plus}, weight_sum={self._weight_sum!r})"
+
+    def as_dict(self) -> dict[int, float]:
+        return dict(self._items)
+
+    def scaled(self, factor: float) -> "WeightedVector":
+        if not (factor > 0.0) or not math.isfinite(factor):
+            raise InvalidWeightError(f"scale factor must be positive, got {factor}")
+        return WeightedVector({e: w * factor for e, w in self._items})
+
+
+@dataclass(frozen=True)
+class GumbelMaxSketch:
+    """k registers: winning element s[j] and value y[j] (sketch.py:118-136)."""
+
+    k: int
+    s: tuple
+    y: tuple
+    fingerprint: int
+
+    def __post_init__(self):
+        if len(self.s) != self.k or len(self.y) != self.k:
+            raise InvalidParameterError(
+                f"register arrays must have length k={self.k}, got {len(self.s)} and {len(self.y)}")
+
+
+@dataclass(frozen=True)
+class GenerationParams:
+    """k and the search increment delta (sketch.py:139-157).  delta only
+    shaped the reference's FastSearch schedule; the device schedule ignores
+    it (output is schedule-independent)."""
+
+    k: int
+    scheme: SeedScheme
+    delta: int | None = None
+
+    def __post_init__(self):
+        if self.k < 1:
+            raise InvalidParameterError(f"k must be >= 1, got {self.k}")
+        if self.delta is None:
+            object.__setattr__(self, "delta", self.k)
+        elif self.delta < 1:
+            raise InvalidParameterError(f"delta must be >= 1, got {self.delta}")
+
+
+def compute_ri(R: int, v: WeightedVector, element: int) -> int:
+    """ceil(R * w / W) (sketch.py:160-169), the reference's release budget."""
+    if R < 0:
+        raise InvalidParameterError(f"R must be >= 0, got {R}")
+    weight = v[element]
+    return math.ceil(R * weight / v.weight_sum)
+
+
+@dataclass
+class SketchBatch:
+    """n sketches as device tensors: y [n, k] float64, s [n, k] int64 holding
+    uint64 element ids (two's complement view), emitted [n] int64 or None."""
+
+    k: int
+    y: torch.Tensor
+    s: torch.Tensor
+    fingerprint: int
+    emitted: torch.Tensor | None = None
+
+    def __len__(self) -> int:
+        return self.y.shape[0]
+
+    def to_sketches(self) -> list[GumbelMaxSketch]:
+        y = self.y.cpu().numpy()
+        s = self.s.cpu().numpy().view(np.uint64)
+        return [GumbelMaxSketch(self.k, tuple(int(x) for x in s[i]), tuple(y[i].tolist()),
+                                self.fingerprint) for i in range(y.shape[0])]
+
+
+def _check_k(k: int) -> None:
+    if k < 1:
+        raise InvalidParameterError(f"k must be >= 1, got {k}")
+
+
+def sketch_csr(ids, weights, offsets, k: int, scheme: SeedScheme, *, exhaustive: bool = False,
+               counted: bool = False, asynchronous: bool = False) -> SketchBatch:
+    """Sketch every CSR vector ids[offsets[v]:offsets[v+1]] on the device.
+
+    ids: uint32/uint64 (or int32/int64 viewed as unsigned) tensor or array;
+    weights: float32/float64; offsets: int64 [n_vec + 1].  Ids must be
+    distinct within a vector (WeightedVector keys).  Device tensors are used
+    in place; host arrays are copied in."""
+    _check_k(k)
+    dev = _device.require_cuda()
+    ids_t = ids if isinstance(ids, torch.Tensor) else torch.from_numpy(_as_id_np(ids))
+    w_t = weights if isinstance(weights, torch.Tensor) else torch.from_numpy(_device.weight_array(weights)[0])
+    off_t = offsets if isinstance(offsets, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(offsets, dtype=np.int64)))
+    ids_t = ids_t.to(dev).contiguous()
+    w_t = w_t.to(dev).contiguous()
+    off_t = off_t.to(dev, dtype=torch.int64).contiguous()
+    n_vec = off_t.numel() - 1
+    y = torch.empty((n_vec, k), dtype=torch.float64, device=dev)
+    s = torch.empty((n_vec, k), dtype=torch.int64, device=dev)
+    em = torch.empty(n_vec, dtype=torch.int64, device=dev) if counted else None
+    flags = (_lib.GM_FLAG_EXHAUSTIVE if exhaustive else 0) | (_lib.GM_FLAG_ASYNC if asynchronous else 0)
+    _device.call("gm_sketch_csr", ids_t.data_ptr(), _device.id_bits_of(ids_t), w_t.data_ptr(),
+                 _device.w_bits_of(w_t), off_t.data_ptr(), n_vec, k, scheme.global_seed,
+                 scheme.stream_salt, flags, y.data_ptr(), s.data_ptr(), _device.ptr(em),
+                 _device.stream_ptr())
+    return SketchBatch(k, y, s, scheme.fingerprint, em)
+
+
+def _as_id_np(ids) -> np.ndarray:
+    a, bits = _device.id_array(ids)
+    return a.view(np.int32 if bits == 32 else np.int64)
+
+
+def sketch_elements(ids, weights, k: int, scheme: SeedScheme, *, exhaustive: bool = False,
+                    into: tuple[torch.Tensor, torch.Tensor] | None = None):
+    """One sketch over a large element set on the device (grid-wide kernel).
+    Ids may repeat only with identical weights.  With ``into=(y, s)`` the
+    elements are folded into an existing device sketch.  Returns
+    (y [k] float64, s [k] int64 view of uint64, emitted)."""
+    _check_k(k)
+    dev = _device.require_cuda()
+    ids_t = ids if isinstance(ids, torch.Tensor) else torch.from_numpy(_as_id_np(ids))
+    w_t = weights if isinstance(weights, torch.Tensor) else torch.from_numpy(_device.weight_array(weights)[0])
+    ids_t = ids_t.to(dev).contiguous()
+    w_t = w_t.to(dev).contiguous()
+    flags = _lib.GM_FLAG_EXHAUSTIVE if exhaustive else 0
+    if into is not None:
+        y, s = into
+        flags |= _lib.GM_FLAG_ACCUMULATE
+    else:
+        y = torch.empty(k, dtype=torch.float64, device=dev)
+        s = torch.empty(k, dtype=torch.int64, device=dev)
+    em = np.zeros(1, dtype=np.int64)
+    _device.call("gm_sketch_elements", ids_t.data_ptr(), _device.id_bits_of(ids_t), w_t.data_ptr(),
+                 _device.w_bits_of(w_t), ids_t.numel(), k, scheme.global_seed, scheme.stream_salt,
+                 flags, y.data_ptr(), s.data_ptr(), em.ctypes.data, _device.stream_ptr())
+    return y, s, int(em[0])
+
+
+def _to_sketch(k, y: np.ndarray, s: np.ndarray, fp: int) -> GumbelMaxSketch:
+    return GumbelMaxSketch(k, tuple(int(x) for x in s.view(np.uint64)), tuple(y.tolist()), fp)
+
+
+def _sketch_vector(v: WeightedVector, params: GenerationParams, exhaustive: bool):
+    if v.n_plus == 0:
+        raise EmptyVectorError("cannot sketch a vector with no positive entries")
+    ids, w = v.arrays()
+    k = params.k
+    if v.n_plus > LARGE_VECTOR:
+        y, s, em = sketch_elements(ids, w, k, params.scheme, exhaustive=exhaustive)
+        return _to_sketch(k, y.cpu().numpy(), s.cpu().numpy(), params.scheme.fingerprint), em
+    _device.require_cuda()
+    bits = 32 if (ids.size and int(ids.max()) < (1 << 32)) else 64
+    ids_h = ids.astype(np.uint32) if bits == 32 else ids
+    off = np.array([0, ids.size], dtype=np.int64)
+    y = np.empty(k, np.float64)
+    s = np.empty(k, np.uint64)
+    em = np.zeros(1, np.int64)
+    flags = _lib.GM_FLAG_EXHAUSTIVE if exhaustive else 0
+    _device.call("gm_sketch_csr_host", ids_h.ctypes.data, bits, w.ctypes.data, 64, off.ctypes.data, 1,
+                 k, params.scheme.global_seed, params.scheme.stream_salt, flags, y.ctypes.data,
+                 s.ctypes.data, em.ctypes.data, _device.stream_ptr())
+    return _to_sketch(k, y, s, params.scheme.fingerprint), int(em[0])
+
+
+def sketch_naive(v: WeightedVector, params: GenerationParams) -> GumbelMaxSketch:
+    """Exhaustive generator: every queue run to k (sketch.py:177-180)."""
+    return sketch_naive_counted(v, params)[0]
+
+
+def sketch_naive_counted(v: WeightedVector, params: GenerationParams):
+    """(sketch, emitted) with emitted = n_plus * k (sketch.py:183-209)."""
+    return _sketch_vector(v, params, exhaustive=True)
+
+
+def sketch_fast(v: WeightedVector, params: GenerationParams) -> GumbelMaxSketch:
+    """Pruned generator; equal to sketch_naive (sketch.py:212-215)."""
+    return sketch_fast_counted(v, params)[0]
+
+
+def sketch_fast_counted(v: WeightedVector, params: GenerationParams):
+    """(sketch, arrivals computed on the device) (sketch.py:218-311)."""
+    return _sketch_vector(v, params, exhaustive=False)
+
+
+def sketch_many(vectors: Sequence[WeightedVector], params: GenerationParams) -> list[GumbelMaxSketch]:
+    """Sketch a list of vectors in one batched launch."""
+    if not vectors:
+        return []
+    for v in vectors:
+        if v.n_plus == 0:
+            raise EmptyVectorError("cannot sketch a vector with no positive entries")
+    ids = np.concatenate([v.arrays()[0] for v in vectors])
+    w = np.concatenate([v.arrays()[1] for v in vectors])
+    off = np.zeros(len(vectors) + 1, dtype=np.int64)
+    off[1:] = np.cumsum([v.n_plus for v in vectors])
+    return sketch_csr(ids, w, off, params.k, params.scheme).to_sketches()
+
+
+def check_compatible(a: GumbelMaxSketch, b: GumbelMaxSketch) -> None:
+    """sketch.py:314-322"""
+    if a.k != b.k:
+        raise MismatchedSketchError(f"register counts differ: {a.k} != {b.k}")
+    if a.fingerprint != b.fingerprint:
+        raise MismatchedSketchError(
+            f"seed-scheme fingerprints differ: {a.fingerprint:#018x} != {b.fingerprint:#018x}")
+
+
+def sketch_to_json(sk: GumbelMaxSketch) -> str:
+    """Versioned record with hex-float registers (sketch.py:325-339)."""
+    record = {"format": SKETCH_FORMAT, "k": sk.k, "fingerprint": f"{sk.fingerprint:#018x}",
+              "s": list(sk.s), "y": [float(value).hex() for value in sk.y]}
+    return json.dumps(record, separators=(",", ":"))
+
+
+def sketch_from_json(text: str) -> GumbelMaxSketch:
+    """sketch.py:342-357"""
+    try:
+        record = json.loads(text)
+    except json.JSONDecodeError as exc:
+        raise MismatchedSketchError(f"not a sketch record: {exc}") from exc
+    if not isinstance(record, dict) or record.get("format") != SKETCH_FORMAT:
+        raise MismatchedSketchError(
+            f"unsupported sketch format {record.get('format') if isinstance(record, dict) else None!r}; "
+            f"expected {SKETCH_FORMAT!r}")
+    k = int(record["k"])
+    s = tuple(int(e) for e in record["s"])
+    y = tuple(float.fromhex(value) for value in record["y"])
+    return GumbelMaxSketch(k, s, y, int(record["fingerprint"], 16))

@@ -1,0 +1,167 @@
+"""Streaming construction (reference stream.py), device-backed.
+
+StreamSketchState keeps the k registers on the device.  stream_update does
+the reference's per-item checks on the host (weight validation, the
+id -> weight dict that raises InconsistentWeightError, duplicate skipping;
+stream.py:58-78) and buffers new items; buffered items are folded into the
+device registers by the grid-wide kernel (gm_sketch_elements with
+GM_FLAG_ACCUMULATE) when the buffer fills or when state is observed.
+Because the registers are a per-register minimum, the result equals the
+reference's one-item-at-a-time walk (stream order only changes work,
+stream.py:1-12); exact ties go to the smaller id (measure zero).
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Iterable, TextIO
+
+import numpy as np
+import torch
+
+from . import _device
+from .errors import IncompleteSketchError, InconsistentWeightError, InvalidParameterError, InvalidWeightError
+from .randgen import MIN_WEIGHT, SeedScheme
+from .sketch import GumbelMaxSketch, sketch_elements
+
+StreamItem = tuple[int, float]
+_MASK64 = (1 << 64) - 1
+FLUSH_ITEMS = 1 << 16
+
+
+class StreamSketchState:
+    """Mutable per-stream sketch under construction (stream.py:30-55)."""
+
+    def __init__(self, k: int, scheme: SeedScheme, skip_duplicates: bool = True):
+        if k < 1:
+            raise InvalidParameterError(f"k must be >= 1, got {k}")
+        self.k = k
+        self.scheme = scheme
+        self.skip_duplicates = skip_duplicates
+        self.weights: dict[int, float] = {}
+        self.emitted = 0
+        self.last_item_emitted = 0
+        self._pending_ids: list[int] = []
+        self._pending_w: list[float] = []
+        self._alias: dict[int, int] = {}  # u64 key -> original id when id not in [0, 2**64)
+        dev = _device.require_cuda()
+        self._y = torch.full((k,), math.inf, dtype=torch.float64, device=dev)
+        self._s = torch.full((k,), -1, dtype=torch.int64, device=dev)
+        self._unset = k
+
+    def _flush(self) -> None:
+        if not self._pending_ids:
+            return
+        ids = np.array([e & _MASK64 for e in self._pending_ids], dtype=np.uint64)
+        w = np.array(self._pending_w, dtype=np.float64)
+        self._pending_ids, self._pending_w = [], []
+        try:
+            _, _, em = sketch_elements(ids, w, self.k, self.scheme, into=(self._y, self._s))
+        except IncompleteSketchError:
+            em = 0
+        self.emitted += em
+        self.last_item_emitted = em
+        self._unset = int(torch.isinf(self._y).sum().item())
+
+    @property
+    def unset_count(self) -> int:
+        self._flush()
+        return self._unset
+
+    @property
+    def prune_enabled(self) -> bool:
+        return self.unset_count == 0
+
+
+def stream_update(state: StreamSketchState, item: StreamItem) -> StreamSketchState:
+    """Fold one (element, weight) item into the sketch (stream.py:58-122)."""
+    element, weight = item
+    element = int(element)
+    weight = float(weight)
+    if not math.isfinite(weight) or weight <= 0.0 or weight < MIN_WEIGHT:
+        raise InvalidWeightError(f"element {element}: weight must be positive and finite, got {weight}")
+    known = state.weights.get(element)
+    if known is not None:
+        if known != weight:
+            raise InconsistentWeightError(
+                f"element {element} reappeared with weight {weight}, previously {known}")
+        if state.skip_duplicates:
+            state.last_item_emitted = 0
+            return state
+    else:
+        state.weights[element] = weight
+    if not 0 <= element <= _MASK64:
+        state._alias[element & _MASK64] = element
+    state._pending_ids.append(element)
+    state._pending_w.append(weight)
+    if len(state._pending_ids) >= FLUSH_ITEMS:
+        state._flush()
+    return state
+
+
+def stream_finalize(state: StreamSketchState) -> GumbelMaxSketch:
+    """Freeze the state; IncompleteSketchError if a register is unset (stream.py:125-140)."""
+    state._flush()
+    y = state._y.cpu().numpy()
+    if state._unset > 0:
+        raise IncompleteSketchError([j for j in range(state.k) if math.isinf(y[j])])
+    s = state._s.cpu().numpy().view(np.uint64)
+    alias = state._alias
+    s_out = tuple(alias.get(int(x), int(x)) for x in s)
+    return GumbelMaxSketch(state.k, s_out, tuple(y.tolist()), state.scheme.fingerprint)
+
+
+def sketch_stream(items: Iterable[StreamItem], k: int, scheme: SeedScheme,
+                  skip_duplicates: bool = True) -> GumbelMaxSketch:
+    """One-pass sketch of an item iterable (stream.py:143-153)."""
+    state = StreamSketchState(k, scheme, skip_duplicates=skip_duplicates)
+    for item in items:
+        stream_update(state, item)
+    return stream_finalize(state)
+
+
+def sketch_pairs(ids, weights, k: int, scheme: SeedScheme, check: bool = True):
+    """Bulk stream of (id, weight) arrays in one device pass.
+
+    With ``check`` the reference's stream checks run vectorised on the host:
+    InvalidWeightError for a bad weight and InconsistentWeightError for an id
+    that reappears with another weight (raised for the first offending item,
+    like stream_update).  Returns a GumbelMaxSketch."""
+    a_ids, _ = _device.id_array(ids)
+    a_w, _ = _device.weight_array(weights)
+    if check and a_ids.size:
+        wd = a_w.astype(np.float64)
+        bad = ~(np.isfinite(wd) & (wd > 0.0) & (wd >= MIN_WEIGHT))
+        first_bad = int(np.argmax(bad)) if bad.any() else None
+        order = np.argsort(a_ids, kind="stable")
+        sid = a_ids[order]
+        sw = a_w[order]
+        same = np.concatenate([[False], sid[1:] == sid[:-1]])
+        grp = np.cumsum(~same) - 1
+        first_w = sw[~same][grp]
+        conflict = order[same & (sw != first_w)]
+        first_conf = int(conflict.min()) if conflict.size else None
+        if first_bad is not None and (first_conf is None or first_bad <= first_conf):
+            raise InvalidWeightError(f"item {first_bad}: weight must be positive and finite, got {a_w[first_bad]}")
+        if first_conf is not None:
+            raise InconsistentWeightError(f"item {first_conf}: element {int(a_ids[first_conf])} reappeared with another weight")
+    y, s, _ = sketch_elements(a_ids, a_w, k, scheme)
+    return GumbelMaxSketch(k, tuple(int(x) for x in s.cpu().numpy().view(np.uint64)),
+                           tuple(y.cpu().numpy().tolist()), scheme.fingerprint)
+
+
+def parse_stream_items(lines: Iterable[str] | TextIO) -> Iterable[StreamItem]:
+    """``element_id weight`` lines (stream.py:156-175)."""
+    for number, raw in enumerate(lines, start=1):
+        line = raw.strip()
+        if not line or line.startswith("#"):
+            continue
+        parts = line.split()
+        if len(parts) != 2:
+            raise InvalidParameterError(f"line {number}: expected 'element_id weight', got {line!r}")
+        try:
+            element = int(parts[0])
+            weight = float(parts[1])
+        except ValueError as exc:
+            raise InvalidParameterError(f"line {number}: {exc}") from exc
+        yield element, weight

@@ -1,0 +1,329 @@
+"""Parity of the CUDA path with the reference (golden fixtures) and the
+CPU oracle.  Every test calls through the C ABI (libgmsketch_b200.so).
+
+Bar (BASELINE.json north_star): argmax indices s bit-exact; register
+values y within 1e-6 relative.  The device log is CUDA's, not glibc's, so
+y may differ by a few ulps: the tests assert YTOL = 1e-12 relative, far
+inside the 1e-6 bar.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2302_05176_b200 as gm
+from oracle import oracle as O
+from paper_2302_05176_b200 import workloads
+from tests.golden_io import hexs, load_json, load_npz, sketch_arrays, vector_case
+
+pytestmark = pytest.mark.gpu
+YTOL = 1e-12
+U64 = (1 << 64) - 1
+
+
+def assert_regs(y, s, wy, ws, tol=YTOL):
+    y = np.asarray(y, np.float64)
+    wy = np.asarray(wy, np.float64)
+    s = np.asarray(s).astype(np.uint64) if np.asarray(s).dtype != np.uint64 else np.asarray(s)
+    assert np.array_equal(s, np.asarray(ws, np.uint64)), f"s differs at {np.nonzero(s != ws)[0][:10]}"
+    rel = np.abs(y - wy) / np.maximum(np.abs(wy), 1e-300)
+    assert float(rel.max()) <= tol, f"max rel y error {rel.max()}"
+
+
+def batch_np(b):
+    return b.y.cpu().numpy(), b.s.cpu().numpy().view(np.uint64)
+
+
+# ---------------------------------------------------------------- K0 RNG
+def test_uniform_open_kats_bit_exact():
+    kats = load_json("rng_kats.json")["uniform_open"]
+    got = gm.uniform_open_batch([k[0] for k in kats], [k[1] for k in kats], [k[2] for k in kats])
+    want = hexs([k[3] for k in kats])
+    assert got.tolist() == want.tolist()
+
+
+def test_uniform_open_random_bit_exact():
+    rng = np.random.default_rng(11)
+    n = 200_000
+    seeds = rng.integers(0, 1 << 63, n, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, n, dtype=np.uint64)
+    el = rng.integers(0, 1 << 63, n, dtype=np.uint64)
+    st = rng.integers(1, 70000, n, dtype=np.uint64)
+    got = gm.uniform_open_batch(seeds, el, st)
+    lib = O.lib()
+    want = np.array([lib.gmo_uniform_open(int(a), int(b), int(c)) for a, b, c in zip(seeds[:20000], el[:20000], st[:20000])])
+    assert got[:20000].tolist() == want.tolist()
+    assert np.all((got > 0) & (got <= 1.0))
+
+
+def test_uniform_can_be_exactly_one():
+    """u = 1.0 when x >> 11 == 2**53 - 1: the device
+    rounding must agree.  Find such a key by inverting nothing: scan the
+    fixture-free property that u <= 1 and equals the oracle on edge keys."""
+    # (x >> 11) * 2**-53 + 2**-54 with x>>11 = 2**53-1 rounds to 1.0 in RN-even
+    assert (2**53 - 1) * 2.0**-53 + 2.0**-54 == 1.0
+
+
+def test_perm_draw_kats_bit_exact():
+    kats = [k for k in load_json("rng_kats.json")["rand_int_between"] if k[4] - k[3] < 65536]
+    # device draw is z + g mod (k - z + 1) keyed on (element, z): map lo..hi onto z..k
+    got = gm.perm_draw_batch([k[0] for k in kats], [k[1] for k in kats], [k[2] for k in kats],
+                             [k[2] + (k[4] - k[3]) for k in kats])
+    want = [k[5] - k[3] + k[2] for k in kats]
+    assert got.tolist() == want
+
+
+def test_perm_draw_random_bit_exact():
+    rng = np.random.default_rng(12)
+    n = 20000
+    ps = rng.integers(0, 1 << 63, n, dtype=np.uint64)
+    el = rng.integers(0, 1 << 63, n, dtype=np.uint64)
+    z = rng.integers(1, 9000, n, dtype=np.uint64)
+    m = rng.integers(1, 65537, n, dtype=np.uint64)
+    ks = z + m - np.uint64(1)
+    got = gm.perm_draw_batch(ps, el, z, ks)
+    want = [O.rand_int_between(int(a), int(b), int(c), int(c), int(d)) for a, b, c, d in zip(ps, el, z, ks)]
+    assert got.tolist() == want
+
+
+# ---------------------------------------------------------------- sketches vs reference fixtures
+def test_sketch_fast_golden_cases():
+    cases = load_json("sketch_cases.json")["vectors"]
+    for case in cases:
+        ids, w = vector_case(case)
+        v = gm.WeightedVector({int(e): float(x) for e, x in zip(ids, w)})
+        sk = gm.sketch_fast(v, gm.GenerationParams(k=case["k"], scheme=gm.SeedScheme(case["seed"])))
+        wy, ws = sketch_arrays(case["fast"])
+        assert_regs(sk.y, np.array(sk.s, np.uint64), wy, ws)
+        assert sk.fingerprint == case["fast"]["fingerprint"]
+
+
+def test_sketch_naive_golden_cases():
+    cases = [c for c in load_json("sketch_cases.json")["vectors"] if c["n"] * c["k"] <= 300_000]
+    for case in cases:
+        ids, w = vector_case(case)
+        v = gm.WeightedVector({int(e): float(x) for e, x in zip(ids, w)})
+        sk, em = gm.sketch_naive_counted(v, gm.GenerationParams(k=case["k"], scheme=gm.SeedScheme(case["seed"])))
+        wy, ws = sketch_arrays(case["fast"])
+        assert_regs(sk.y, np.array(sk.s, np.uint64), wy, ws)
+        assert em == case["n"] * case["k"]
+
+
+def test_batched_golden_cases_one_launch():
+    cases = load_json("sketch_cases.json")["vectors"]
+    by_k = {}
+    for c in cases:
+        by_k.setdefault((c["k"], c["seed"]), []).append(c)
+    # one launch per case group with equal (k, seed); also one mixed big batch at k=96
+    for (k, seed), group in by_k.items():
+        ids = np.concatenate([vector_case(c)[0] for c in group])
+        w = np.concatenate([vector_case(c)[1] for c in group])
+        off = np.zeros(len(group) + 1, np.int64)
+        off[1:] = np.cumsum([c["n"] for c in group])
+        y, s = batch_np(gm.sketch_csr(ids, w, off, k, gm.SeedScheme(seed)))
+        for i, c in enumerate(group):
+            assert_regs(y[i], s[i], *sketch_arrays(c["fast"]))
+
+
+def test_stream_golden_cases():
+    for case in load_json("sketch_cases.json")["streams"]:
+        items = list(zip(case["ids"], hexs(case["w"]).tolist()))
+        sk = gm.sketch_stream(items, case["k"], gm.SeedScheme(case["seed"]))
+        wy, ws = sketch_arrays(case["sketch"])
+        assert_regs(sk.y, np.array([int(x) & U64 for x in sk.s], np.uint64), wy, ws)
+        assert tuple(sk.s) == tuple(case["sketch"]["s"])  # original (possibly huge) ids come back
+
+
+def test_merge_golden_cases():
+    for case in load_json("sketch_cases.json")["merges"]:
+        parts = [gm.GumbelMaxSketch(case["k"], tuple(p["s"]), tuple(hexs(p["y"]).tolist()), p["fingerprint"])
+                 for p in case["parts"]]
+        merged = gm.merge(parts)
+        wy, ws = sketch_arrays(case["merged"])
+        assert list(merged.y) == wy.tolist()  # merge is pure comparison: bit-exact
+        assert np.array_equal(np.array(merged.s, np.uint64), ws)
+
+
+def test_bench_golden():
+    """test_bench.py:67-82: seed 2024, k=16 -> 9 matches, J=0.5625, c=1.76291929033662."""
+    g = load_json("bench_golden.json")
+    params = gm.GenerationParams(k=16, scheme=gm.SeedScheme(2024))
+    sks = [gm.sketch_fast(gm.WeightedVector({e: x for e, x in vec}), params) for vec in g["vectors"]]
+    sim = gm.estimate_jaccard_p(sks[0], sks[1])
+    assert sim.matches == 9 and sim.value == 0.5625
+    assert gm.estimate_cardinality(sks[2]).value == pytest.approx(1.76291929033662, rel=1e-12)
+    for sk, want in zip(sks, g["sketches"]):
+        assert_regs(sk.y, np.array(sk.s, np.uint64), *sketch_arrays(want))
+
+
+def test_config1_golden():
+    g = load_npz("config1.npz")
+    b = gm.sketch_csr(g["ids"].astype(np.uint32), g["w"], np.array([0, g["ids"].size]), int(g["k"]),
+                      gm.SeedScheme(int(g["seed"])))
+    y, s = batch_np(b)
+    assert_regs(y[0], s[0], g["y"], g["s"])
+    # the grid-wide kernel agrees too
+    y2, s2, _ = gm.sketch_elements(g["ids"].astype(np.uint32), g["w"], int(g["k"]), gm.SeedScheme(int(g["seed"])))
+    assert_regs(y2.cpu().numpy(), s2.cpu().numpy().view(np.uint64), g["y"], g["s"])
+
+
+def test_config2_sample_golden():
+    g = load_npz("config2_sample.npz")
+    y, s = batch_np(gm.sketch_csr(g["ids"], g["w"], g["offsets"], int(g["k"]), gm.SeedScheme(int(g["seed"]))))
+    for i in range(y.shape[0]):
+        assert_regs(y[i], s[i], g["y"][i], g["s"][i])
+
+
+# ---------------------------------------------------------------- full-size configs vs the oracle
+def test_config2_full_vs_oracle():
+    ids, w, off, k, seed = workloads.config2()
+    b = gm.sketch_csr(ids, w, off, k, gm.SeedScheme(seed), counted=True)
+    y, s = batch_np(b)
+    rc, yo, so, _ = O.sketch_csr(ids.astype(np.uint64), w.astype(np.float64), off, k, seed, mode=0, threads=8)
+    assert rc == 0
+    assert_regs(y, s, yo, so)
+    # estimator batch: matches of pairs (2i, 2i+1)
+    sa = torch.from_numpy(s[0::2].view(np.int64)).cuda()
+    sb = torch.from_numpy(s[1::2].view(np.int64)).cuda()
+    ba = gm.SketchBatch(k, b.y[0::2].contiguous(), sa, b.fingerprint)
+    bb = gm.SketchBatch(k, b.y[1::2].contiguous(), sb, b.fingerprint)
+    m = gm.estimate_jaccard_p_batch(ba, bb).cpu().numpy()
+    assert m.tolist() == np.sum(so[0::2] == so[1::2], axis=1).tolist()
+
+
+def test_config3_subset_vs_oracle():
+    ids, w, off, k, seed = workloads.config3(n_vectors=3000)
+    y, s = batch_np(gm.sketch_csr(ids, w, off, k, gm.SeedScheme(seed)))
+    rc, yo, so, _ = O.sketch_csr(ids.astype(np.uint64), w.astype(np.float64), off, k, seed, mode=0, threads=8)
+    assert rc == 0
+    assert_regs(y, s, yo, so)
+
+
+def test_config4_prefix_vs_oracle():
+    ids, w, k, seed = workloads.config4(n_pairs=2_000_000, n_keys=10**7)
+    y, s, _ = gm.sketch_elements(ids, w, k, gm.SeedScheme(seed))
+    rc, yo, so, _, _ = O.sketch_stream(ids, w.astype(np.float64), k, seed)
+    assert rc == 0
+    assert_regs(y.cpu().numpy(), s.cpu().numpy().view(np.uint64), yo, so)
+
+
+def test_config5_prefix_vs_oracle():
+    n = 5_000_000
+    rng = np.random.default_rng(5)
+    w = rng.lognormal(0.0, 2.0, n).astype(np.float32)
+    ids = np.arange(n, dtype=np.uint32)
+    y, s, _ = gm.sketch_elements(ids, w, 8192, gm.SeedScheme(1))
+    rc, yo, so, _, _ = O.sketch_stream(ids.astype(np.uint64), w.astype(np.float64), 8192, 1)
+    assert rc == 0
+    assert_regs(y.cpu().numpy(), s.cpu().numpy().view(np.uint64), yo, so)
+
+
+# ---------------------------------------------------------------- size-independent properties at full size
+def test_partition_law_large():
+    """sketch(whole) == merge(sketch(part) for parts) on 2**26 elements (k=8192)."""
+    n = 1 << 26
+    rng = np.random.default_rng(55)
+    w = torch.from_numpy(rng.lognormal(0.0, 2.0, n).astype(np.float32)).cuda()
+    ids = torch.arange(n, dtype=torch.int32, device="cuda")
+    sc = gm.SeedScheme(1)
+    yw, sw, _ = gm.sketch_elements(ids, w, 8192, sc)
+    parts = [gm.sketch_elements(ids[a:b], w[a:b], 8192, sc)[:2] for a, b in
+             [(0, n // 3), (n // 3, n // 2), (n // 2, n)]]
+    ym, sm = gm.merge_arrays(torch.stack([p[0] for p in parts]), torch.stack([p[1] for p in parts]))
+    assert torch.equal(sm, sw)
+    assert torch.equal(ym, yw)  # same arrivals, same arithmetic: bit-identical
+    # idempotence and duplicates: the whole set twice is the same sketch
+    y2, s2, _ = gm.sketch_elements(torch.cat([ids, ids[: n // 4]]), torch.cat([w, w[: n // 4]]), 8192, sc)
+    assert torch.equal(s2, sw) and torch.equal(y2, yw)
+
+
+def test_csr_vs_elements_kernels_agree():
+    ids, w, off, k, seed = workloads.config3(n_vectors=200)
+    y, s = batch_np(gm.sketch_csr(ids, w, off, k, gm.SeedScheme(seed)))
+    for v in range(0, 200, 37):
+        a, b = off[v], off[v + 1]
+        y2, s2, _ = gm.sketch_elements(ids[a:b], w[a:b], k, gm.SeedScheme(seed))
+        assert_regs(y2.cpu().numpy(), s2.cpu().numpy().view(np.uint64), y[v], s[v], tol=0.0)
+
+
+# ---------------------------------------------------------------- edge cases
+def test_single_element_owns_every_register():
+    for k in (1, 3, 64, 1024, 4096):
+        v = gm.WeightedVector({5: 1.0})
+        sk = gm.sketch_fast(v, gm.GenerationParams(k=k, scheme=gm.SeedScheme(77)))
+        assert set(sk.s) == {5}
+        t, srv = O.run_queue_full(77, O.DEFAULT_STREAM_SALT, 5, 1.0, k)
+        want = np.empty(k)
+        want[srv - 1] = t
+        assert_regs(sk.y, np.array(sk.s, np.uint64), want, np.full(k, 5, np.uint64))
+
+
+def test_heavy_and_tiny_weights():
+    rng = np.random.default_rng(3)
+    for n, k in [(3, 512), (20, 2048), (50, 8192), (400, 65536)]:
+        ids = rng.choice(10**9, n, replace=False).astype(np.uint64) + 1
+        w = np.exp(rng.normal(0, 6, n))
+        w[0] = 1e-300
+        w[-1] = 1e300 / n
+        rc, yo, so, _ = O.sketch_fast(np.sort(ids), w[np.argsort(ids)], k, 9)
+        y, s = batch_np(gm.sketch_csr(ids, w, np.array([0, n]), k, gm.SeedScheme(9)))
+        assert_regs(y[0], s[0], yo, so)
+
+
+def test_u64_ids_and_zero():
+    ids = np.array([0, 1, (1 << 64) - 1, 1 << 63, 12345678901234567], dtype=np.uint64)
+    w = np.array([0.5, 1.5, 2.0, 0.25, 1.0])
+    order = np.argsort(ids)
+    rc, yo, so, _ = O.sketch_fast(ids[order], w[order], 97, 3)
+    y, s = batch_np(gm.sketch_csr(ids, w, np.array([0, 5]), 97, gm.SeedScheme(3)))
+    assert_regs(y[0], s[0], yo, so)
+
+
+def test_exhaustive_equals_fast_and_counts():
+    ids, w, off, k, seed = workloads.config2(n_vectors=16)
+    sc = gm.SeedScheme(seed)
+    bf = gm.sketch_csr(ids, w, off, k, sc, counted=True)
+    bn = gm.sketch_csr(ids, w, off, k, sc, exhaustive=True, counted=True)
+    assert torch.equal(bf.s, bn.s) and torch.equal(bf.y, bn.y)
+    assert bn.emitted.cpu().numpy().tolist() == (np.diff(off) * k).tolist()
+    assert int(bf.emitted.sum()) < int(bn.emitted.sum()) / 20
+
+
+def test_errors_map_to_reference_classes():
+    sc = gm.SeedScheme(1)
+    with pytest.raises(gm.InvalidWeightError):
+        gm.sketch_csr(np.array([1, 2], np.uint32), np.array([1.0, -1.0]), np.array([0, 2]), 8, sc)
+    with pytest.raises(gm.InvalidWeightError):
+        gm.sketch_csr(np.array([1, 2], np.uint32), np.array([1.0, math.nan]), np.array([0, 2]), 8, sc)
+    with pytest.raises(gm.EmptyVectorError):
+        gm.sketch_csr(np.array([1, 2], np.uint32), np.array([1.0, 1.0]), np.array([0, 2, 2]), 8, sc)
+    with pytest.raises(gm.InvalidParameterError):
+        gm.sketch_csr(np.array([1], np.uint32), np.array([1.0]), np.array([0, 1]), 70000, sc)
+    with pytest.raises(gm.EmptyVectorError):
+        gm.sketch_fast(gm.WeightedVector({}), gm.GenerationParams(k=4, scheme=sc))
+    with pytest.raises(gm.InconsistentWeightError):
+        gm.sketch_pairs(np.array([1, 2, 1], np.uint64), np.array([0.5, 1.0, 0.75]), 4, sc)
+    with pytest.raises(gm.InvalidWeightError):
+        gm.sketch_elements(np.array([1, 2], np.uint32), np.array([1.0, 0.0]), 8, sc)
+    with pytest.raises(gm.MismatchedSketchError):
+        gm.merge([])
+    # the library recovers after a data error
+    sk = gm.sketch_fast(gm.WeightedVector({1: 1.0}), gm.GenerationParams(k=4, scheme=sc))
+    assert sk.s == (1, 1, 1, 1)
+
+
+def test_stream_state_api():
+    sc = gm.SeedScheme(77)
+    st = gm.StreamSketchState(2, sc)
+    gm.stream_update(st, (4, 1.5))
+    assert st.unset_count == 0 and st.prune_enabled
+    assert gm.stream_finalize(st).s == (4, 4)
+    st = gm.StreamSketchState(3, sc)
+    with pytest.raises(gm.IncompleteSketchError) as ei:
+        gm.stream_finalize(st)
+    assert ei.value.unset_registers == [0, 1, 2]
+    st = gm.StreamSketchState(4, sc)
+    gm.stream_update(st, (1, 0.5))
+    with pytest.raises(gm.InconsistentWeightError):
+        gm.stream_update(st, (1, 0.75))
