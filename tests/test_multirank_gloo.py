@@ -1,0 +1,82 @@
+"""world_size-2 gloo runs of the multi-GPU host logic on CPU.
+
+Per-rank sketches come from the CPU oracle (this container has no GPU);
+what is under test is the sharding and the register exchange in
+paper_2302_05176_b200/shard.py: contiguous element shards, all-gather of
+k registers in rank order, and the rank-order min-merge reproducing the
+whole-stream sketch (partition law, test_estimate.py:174-199).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+from paper_2302_05176_b200 import shard, workloads
+
+WORLD = 2
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _stream_worker(rank, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    ids, w, k, seed = workloads.config4(n_pairs=200_000, n_keys=50_000)
+    k = 256
+    lo, hi = shard.element_range(ids.size, WORLD, rank)
+    rc, y, s, _, _ = O.sketch_stream(ids[lo:hi], w[lo:hi].astype(np.float64), k, seed)
+    assert rc == 0
+    ya, sa = shard.gather_registers(torch.from_numpy(y), torch.from_numpy(s.view(np.int64)))
+    ym, sm = O.merge(ya.numpy(), sa.numpy().view(np.uint64))
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), y=ym, s=sm)
+    dist.destroy_process_group()
+
+
+def _csr_worker(rank, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    ids, w, off, k, seed = workloads.config3(n_vectors=300)
+    v0, v1 = shard.vector_ranges(off, WORLD)[rank]
+    lo, hi = off[v0], off[v1]
+    rc, y, s, _ = O.sketch_csr(ids[lo:hi].astype(np.uint64), w[lo:hi].astype(np.float64), off[v0:v1 + 1] - lo,
+                               k, seed, mode=0)
+    assert rc == 0
+    # no data-path collective: only the element count is all-reduced for the report
+    n = torch.tensor([int(hi - lo)], dtype=torch.int64)
+    dist.all_reduce(n)
+    np.savez(os.path.join(out_dir, f"csr{rank}.npz"), y=y, s=s, n=n.numpy(), v0=v0, v1=v1)
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_stream_shards_merge_to_whole(tmp_path):
+    mp.spawn(_stream_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, join=True)
+    ids, w, _, seed = workloads.config4(n_pairs=200_000, n_keys=50_000)
+    rc, yw, sw, _, _ = O.sketch_stream(ids, w.astype(np.float64), 256, seed)
+    assert rc == 0
+    for r in range(WORLD):
+        d = np.load(tmp_path / f"rank{r}.npz")
+        assert np.array_equal(d["s"], sw)
+        assert d["y"].tolist() == yw.tolist()
+
+
+@pytest.mark.timeout(300)
+def test_vector_shards_cover_batch(tmp_path):
+    mp.spawn(_csr_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, join=True)
+    ids, w, off, k, seed = workloads.config3(n_vectors=300)
+    rc, yw, sw, _ = O.sketch_csr(ids.astype(np.uint64), w.astype(np.float64), off, k, seed, mode=0)
+    parts = [np.load(tmp_path / f"csr{r}.npz") for r in range(WORLD)]
+    assert int(parts[0]["n"][0]) == int(off[-1])
+    y = np.concatenate([p["y"] for p in parts])
+    s = np.concatenate([p["s"] for p in parts])
+    assert np.array_equal(s, sw) and y.tolist() == yw.tolist()
