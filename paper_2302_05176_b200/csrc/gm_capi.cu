@@ -48,6 +48,8 @@ struct Workspace {
   size_t heavy_cap = 0;
   u32* dense = nullptr;
   size_t dense_cap = 0;
+  u32* resume = nullptr;
+  size_t resume_cap = 0;
   void* stage = nullptr;                   // device staging for *_host calls
   size_t stage_cap = 0;
 };
@@ -131,9 +133,8 @@ int num_sms() {
 }
 
 size_t csr_smem_bytes(u32 k) {
-  const size_t pool = k <= DENSE_SMEM_MAX_K ? std::max((size_t)LIGHT_CAP * NT, (size_t)NWARP * k)
-                                            : (size_t)LIGHT_CAP * NT;
-  return (size_t)k * sizeof(Reg) + pool * 4 + NWARP * 32 * 8 + NWARP * 32 * 4 + HEAVY_LIST * 4;
+  return (size_t)k * sizeof(Reg) + csr_pool_words(k) * 4 + RCAP * sizeof(ResumeRec) + NWARP * 32 * 8 +
+         NWARP * 32 * 4 + HCAP * 4;
 }
 
 template <class IdT, class WT>
@@ -152,8 +153,13 @@ int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n
     auto key = std::make_pair((const void*)kern, smem);
     auto it = cache.find(key);
     if (it == cache.end()) {
-      if (smem <= 232448) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int dev = 0, optin = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+      if (smem <= (size_t)optin) {
+        // one limit per function (the device maximum), so launches with a
+        // smaller k never lower it under a larger k's requirement
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
       }
       it = cache.emplace(key, per_sm).first;
@@ -164,14 +170,17 @@ int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n
   int64_t grid = (int64_t)per_sm * num_sms();
   if (grid > n_vec) grid = n_vec;
   u32* dense = nullptr;
-  if (k > DENSE_SMEM_MAX_K) {
+  if (!csr_dense_in_smem(k)) {
     int rc = grow(&ws->dense, &ws->dense_cap, (size_t)grid * NWARP * k, st);
     if (rc) return rc;
     dense = ws->dense;
   }
+  int rc = grow(&ws->resume, &ws->resume_cap, (size_t)grid * RCAP * CAP, st);
+  if (rc) return rc;
   CK(cudaMemsetAsync(ws->counters, 0, sizeof(int), st));
   kern<<<(unsigned)grid, NT, smem, st>>>((const IdT*)ids, (const WT*)w, offsets, n_vec, k, useed,
-                                         pseed, y, s, em, ws->counters, dense, ws->err, attempt0);
+                                         pseed, y, s, em, ws->counters, dense, ws->resume, ws->err,
+                                         attempt0);
   CK(cudaGetLastError());
   return GM_OK;
 }
@@ -306,6 +315,7 @@ int gm_sketch_csr(const void* ids, int id_bits, const void* w, int w_bits, const
                   uint32_t flags, double* y_out, uint64_t* s_out, int64_t* emitted_out,
                   void* stream) {
   g_msg[0] = 0;
+  (void)cudaGetLastError();
   int rc = check_common(id_bits, w_bits, k);
   if (rc) return rc;
   if (n_vec < 0) return fail(GM_ERR_INVALID_PARAMETER, "n_vec must be >= 0");
@@ -339,6 +349,7 @@ int gm_sketch_csr_host(const void* ids, int id_bits, const void* w, int w_bits,
                        uint64_t stream_salt, uint32_t flags, double* y_out, uint64_t* s_out,
                        int64_t* emitted_out, void* stream) {
   g_msg[0] = 0;
+  (void)cudaGetLastError();
   int rc = check_common(id_bits, w_bits, k);
   if (rc) return rc;
   if (n_vec < 0) return fail(GM_ERR_INVALID_PARAMETER, "n_vec must be >= 0");
@@ -377,6 +388,7 @@ int gm_sketch_elements(const void* ids, int id_bits, const void* w, int w_bits, 
                        int32_t k, uint64_t global_seed, uint64_t stream_salt, uint32_t flags,
                        double* y_io, uint64_t* s_io, int64_t* emitted_out, void* stream) {
   g_msg[0] = 0;
+  (void)cudaGetLastError();
   int rc = check_common(id_bits, w_bits, k);
   if (rc) return rc;
   if (n < 0) return fail(GM_ERR_INVALID_PARAMETER, "n must be >= 0");
@@ -406,6 +418,7 @@ int gm_sketch_elements_host(const void* ids, int id_bits, const void* w, int w_b
                             uint32_t flags, double* y_io, uint64_t* s_io, int64_t* emitted_out,
                             void* stream) {
   g_msg[0] = 0;
+  (void)cudaGetLastError();
   int rc = check_common(id_bits, w_bits, k);
   if (rc) return rc;
   if (n < 0) return fail(GM_ERR_INVALID_PARAMETER, "n must be >= 0");
@@ -442,6 +455,7 @@ int gm_sketch_elements_host(const void* ids, int id_bits, const void* w, int w_b
 int gm_merge(const double* y_in, const uint64_t* s_in, int64_t n_sk, int32_t k, double* y_out,
              uint64_t* s_out, void* stream) {
   g_msg[0] = 0;
+  (void)cudaGetLastError();
   if (n_sk < 1) return fail(GM_ERR_MISMATCHED, "MismatchedSketchError: cannot merge an empty list of sketches");
   if (k < 1) return fail(GM_ERR_INVALID_PARAMETER, "k must be >= 1");
   const unsigned grid = (unsigned)std::min<int64_t>(((int64_t)k + 255) / 256, 4096);
@@ -453,6 +467,7 @@ int gm_merge(const double* y_in, const uint64_t* s_in, int64_t n_sk, int32_t k, 
 int gm_match_count(const uint64_t* s_a, const uint64_t* s_b, int64_t n_pairs, int32_t k,
                    int32_t* matches, void* stream) {
   g_msg[0] = 0;
+  (void)cudaGetLastError();
   if (k < 1) return fail(GM_ERR_INVALID_PARAMETER, "k must be >= 1");
   if (n_pairs <= 0) return GM_OK;
   match_count_kernel<<<(unsigned)n_pairs, 256, 0, (cudaStream_t)stream>>>(s_a, s_b, n_pairs, (u32)k, matches);
@@ -463,6 +478,7 @@ int gm_match_count(const uint64_t* s_a, const uint64_t* s_b, int64_t n_pairs, in
 int gm_uniform_open_batch(const uint64_t* global_seeds, const uint64_t* elements,
                           const uint64_t* steps, int64_t n, double* out, void* stream) {
   g_msg[0] = 0;
+  (void)cudaGetLastError();
   if (n <= 0) return GM_OK;
   uniform_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(global_seeds, elements, steps, n, out);
   CK(cudaGetLastError());
@@ -473,6 +489,7 @@ int gm_uniform_open_batch(const uint64_t* global_seeds, const uint64_t* elements
 int gm_perm_draw_batch(const uint64_t* perm_seeds, const uint64_t* elements, const uint64_t* steps,
                        const uint32_t* ks, int64_t n, uint32_t* out, void* stream) {
   g_msg[0] = 0;
+  (void)cudaGetLastError();
   if (n <= 0) return GM_OK;
   randint_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(perm_seeds, elements, steps, ks, n, out);
   CK(cudaGetLastError());
@@ -482,6 +499,7 @@ int gm_perm_draw_batch(const uint64_t* perm_seeds, const uint64_t* elements, con
 
 int gm_probe_arrival_rate(int64_t n_threads, int32_t iters, int32_t k, double* sink, void* stream) {
   g_msg[0] = 0;
+  (void)cudaGetLastError();
   if (k < 2 || k > 65536 || iters < 1 || n_threads < NT)
     return fail(GM_ERR_INVALID_PARAMETER, "bad probe arguments");
   arrival_probe_kernel<<<(unsigned)(n_threads / NT), NT, 0, (cudaStream_t)stream>>>(
@@ -494,6 +512,7 @@ int gm_count_arrivals_csr(const void* ids, int id_bits, const void* w, int w_bit
                           const int64_t* offsets, int64_t n_vec, int32_t k, uint64_t global_seed,
                           const double* tau, unsigned long long* counts, void* stream) {
   g_msg[0] = 0;
+  (void)cudaGetLastError();
   int rc = check_common(id_bits, w_bits, k);
   if (rc) return rc;
   if (n_vec <= 0) return GM_OK;

@@ -20,9 +20,6 @@ namespace gmk {
 
 constexpr int NT = 256;           // threads per CTA
 constexpr int NWARP = NT / 32;
-constexpr int LIGHT_CAP = 32;     // light-walker list entries per thread
-constexpr int HEAVY_LIST = 512;   // per-CTA heavy-element list
-constexpr u32 DENSE_SMEM_MAX_K = 2048;
 
 // device-side error word: code in the low 32 bits (gm error enum), the
 // first offending vector/element index in the high 32 bits
@@ -52,50 +49,77 @@ __device__ __forceinline__ double pass_tau(double W, u32 k, int attempt) {
   return (log((double)k) + c) / W;
 }
 
+struct ResumeRec {
+  u32 elem;  // local element index
+  u32 z;     // accepted arrivals
+  u32 nl;    // live permutation entries (stored in the CTA's global slot)
+  u32 pad;
+  double b;  // time of the last accepted arrival
+};
+
 struct CsrSmem {
   int unset;
-  int next_light;
+  int grab;
   int n_heavy;
-  int heavy_overflow;
+  int heavy_ovf;
+  int n_resume;
+  int resume_ovf;
   int vec;
-  u32 stamp;
+  int pad;
   unsigned long long emitted;
   double wsum[NWARP];
 };
 
+constexpr int CAP = 40;        // lane-walker permutation entries per thread
+constexpr int HCAP = 1024;     // heaviest-first list
+constexpr int RCAP = 256;      // warp-phase records
+constexpr double LPT_DEPTH = 12.0;   // expected depth that goes first
+constexpr double DEEP_DEPTH = 48.0;  // expected depth that goes straight to the warp walker
+
+__host__ __device__ constexpr size_t csr_pool_words(u32 k) {
+  return (size_t)CAP * NT;  // lane maps; the warp phase reuses it for dense arrays when they fit
+}
+__host__ __device__ constexpr bool csr_dense_in_smem(u32 k) { return (size_t)NWARP * k <= (size_t)CAP * NT; }
+
 // K1.  Dynamic shared memory layout:
-//   Reg regs[k] | union{ u32 light[LIGHT_CAP][NT], u32 dense[NWARP][k] (k <= DENSE_SMEM_MAX_K) }
-//   | double scan[NWARP][32] | int prov[NWARP][32] | u32 heavy[HEAVY_LIST]
+//   Reg regs[k] | u32 pool[CAP*NT] (lane maps, then per-warp dense arrays)
+//   | ResumeRec rec[RCAP] | double scan[NWARP][32] | int prov[NWARP][32] | u32 heavy[HCAP]
+// Per vector and pass: (1) classify elements by expected depth k*w*tau
+// into a heaviest-first list and a straight-to-warp list, (2) flattened
+// lane phase (one step per lane per iteration, immediate refill), (3) warp
+// phase for elements whose permutation list overflowed (resumed) or that
+// are expected to be deep, (4) unset check -> next pass with a larger tau.
 template <class IdT, class WT>
 __global__ void __launch_bounds__(NT, 3)
     csr_sketch_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts,
                       const int64_t* __restrict__ offsets, int64_t n_vec, u32 k, u64 useed,
                       u64 pseed, double* __restrict__ y_out, u64* __restrict__ s_out,
                       int64_t* __restrict__ emitted_out, int* __restrict__ vec_counter,
-                      u32* __restrict__ dense_global, unsigned long long* __restrict__ err,
-                      int attempt0) {
+                      u32* __restrict__ dense_global, u32* __restrict__ resume_global,
+                      unsigned long long* __restrict__ err, int attempt0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ CsrSmem S;
+  const unsigned FULL = 0xFFFFFFFFu;
   Reg* regs = reinterpret_cast<Reg*>(smem_raw);
   u32* pool = reinterpret_cast<u32*>(smem_raw + (size_t)k * sizeof(Reg));
-  const bool dense_in_smem = k <= DENSE_SMEM_MAX_K;
-  const size_t pool_words = dense_in_smem ? max((size_t)LIGHT_CAP * NT, (size_t)NWARP * k)
-                                          : (size_t)LIGHT_CAP * NT;
-  double* scan_all = reinterpret_cast<double*>(pool + pool_words);
+  ResumeRec* rec = reinterpret_cast<ResumeRec*>(pool + csr_pool_words(k));
+  double* scan_all = reinterpret_cast<double*>(rec + RCAP);
   int* prov_all = reinterpret_cast<int*>(scan_all + NWARP * 32);
   u32* heavy = reinterpret_cast<u32*>(prov_all + NWARP * 32);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  u32* dense = dense_in_smem ? pool + (size_t)warp * k
-                             : dense_global + ((size_t)blockIdx.x * NWARP + warp) * k;
-  if (tid == 0) S.stamp = 0;
-  // dense stamps start clean
-  if (dense_in_smem) {
-    // (re-initialised lazily below when the stamp wraps)
-  } else {
+  const bool dense_smem = csr_dense_in_smem(k);
+  u32* dense = dense_smem ? pool + (size_t)warp * k
+                          : dense_global + ((size_t)blockIdx.x * NWARP + warp) * k;
+  u32* rmaps = resume_global + (size_t)blockIdx.x * RCAP * CAP;
+  // warp stamps: >= 0x8000 so stale lane-map words (pos < 0x8000) never match
+  const u32 stamp_lo = dense_smem ? 0x8000u : 1u;
+  u32 stamp = stamp_lo - 1;
+  if (!dense_smem)
     for (u32 i = lane; i < k; i += 32) dense[i] = 0;
-  }
-  __syncthreads();
+  double* scan = scan_all + warp * 32;
+  int* prov = prov_all + warp * 32;
+  u32* mymap = pool + tid;
 
   for (;;) {
     if (tid == 0) S.vec = atomicAdd(vec_counter, 1);
@@ -113,7 +137,7 @@ __global__ void __launch_bounds__(NT, 3)
       ws += w;
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) ws += __shfl_xor_sync(0xFFFFFFFFu, ws, o);
+    for (int o = 16; o; o >>= 1) ws += __shfl_xor_sync(FULL, ws, o);
     if (lane == 0) S.wsum[warp] = ws;
     for (u32 j = tid; j < k; j += NT) {
       regs[j].y = INF_BITS;
@@ -127,83 +151,143 @@ __global__ void __launch_bounds__(NT, 3)
     double W = 0.0;
 #pragma unroll
     for (int i = 0; i < NWARP; ++i) W += S.wsum[i];
-    if (n == 0) {
-      if (tid == 0) raise_error(err, 1u, (u64)v);
-    }
+    if (n == 0 && tid == 0) raise_error(err, 1u, (u64)v);
 
     u32 emitted = 0;
     for (int attempt = attempt0; n > 0; ++attempt) {
       const double tau = pass_tau(W, k, attempt);
-      const double light_w = 8.0 / ((double)k * tau);  // expected depth k*w*tau < 8
+      const double kt = (double)k * tau;  // expected depth = k * w * tau
+      const double lpt_w = LPT_DEPTH / kt, deep_w = DEEP_DEPTH / kt;
       if (tid == 0) {
-        S.next_light = 0;
+        S.grab = 0;
         S.n_heavy = 0;
-        S.heavy_overflow = 0;
+        S.heavy_ovf = 0;
+        S.n_resume = 0;
+        S.resume_ovf = 0;
       }
       __syncthreads();
-      // ---- light phase: one thread per element, dynamic grab
-      u32* mymap = pool + tid;
-      for (;;) {
-        const int i = atomicAdd(&S.next_light, 1);
-        if (i >= n) break;
+      // (1) classify
+      for (int i = tid; i < n; i += NT) {
         const double w = load_w(wts, lo + i);
-        bool ok = false;
-        if (w < light_w) {
-          ok = walk_light<true>(load_id(ids, lo + i), w, tau, k, useed, pseed, mymap, NT,
-                                LIGHT_CAP, regs, &S.unset, emitted);
-        }
-        if (!ok) {
+        if (w >= deep_w) {
+          const int r = atomicAdd(&S.n_resume, 1);
+          if (r < RCAP) {
+            rec[r].elem = (u32)i;
+            rec[r].z = 0;
+            rec[r].nl = 0;
+            rec[r].b = 0.0;
+          } else {
+            S.resume_ovf = 1;
+          }
+        } else if (w >= lpt_w) {
           const int h = atomicAdd(&S.n_heavy, 1);
-          if (h < HEAVY_LIST)
-            heavy[h] = (u32)i;
-          else
-            S.heavy_overflow = 1;
+          if (h < HCAP) heavy[h] = (u32)i;
+          else S.heavy_ovf = 1;
         }
       }
       __syncthreads();
-      // ---- heavy phase: one warp per element
-      const bool all = S.heavy_overflow != 0;
-      const int nh = all ? n : min(S.n_heavy, HEAVY_LIST);
-      if (dense_in_smem) {
-        for (u32 i = tid; i < (u32)NWARP * k; i += NT) pool[i] = 0;
-        __syncthreads();
+      const int nh = min(S.n_heavy, HCAP);
+      const bool hovf = S.heavy_ovf != 0;
+      // (2) flattened lane phase
+      {
+        LaneWalk L;
+        int cur = -1;
+        bool done = false;
+        for (;;) {
+          if (cur < 0 && !done) {
+            for (;;) {
+              const int q = atomicAdd(&S.grab, 1);
+              if (q < nh) {
+                cur = (int)heavy[q];
+                break;
+              }
+              const int i = q - nh;
+              if (i >= n) {
+                done = true;
+                break;
+              }
+              const double w = load_w(wts, lo + i);
+              if (w >= deep_w || (w >= lpt_w && !hovf)) continue;  // listed elsewhere
+              cur = i;
+              break;
+            }
+            if (cur >= 0) lane_start(L, load_id(ids, lo + cur), load_w(wts, lo + cur), k, useed, pseed);
+          }
+          if (__all_sync(FULL, cur < 0)) break;
+          if (cur >= 0) {
+            if (L.t > tau) {
+              emitted += L.z + 1;
+              cur = -1;
+            } else if (L.nl == CAP) {  // list full: hand over to the warp phase
+              const int r = atomicAdd(&S.n_resume, 1);
+              if (r < RCAP) {
+                rec[r].elem = (u32)cur;
+                rec[r].z = L.z;
+                rec[r].nl = (u32)CAP;
+                rec[r].b = L.b;
+                for (int e = 0; e < CAP; ++e) rmaps[(size_t)r * CAP + e] = mymap[e * NT];
+              } else {
+                S.resume_ovf = 1;
+              }
+              emitted += L.z;
+              cur = -1;
+            } else {
+              lane_accept<true>(L, k, mymap, NT, regs, &S.unset);
+              if (L.z == k) {
+                emitted += k;
+                cur = -1;
+              }
+            }
+          }
+        }
       }
-      if (tid == 0) S.next_light = 0;
       __syncthreads();
-      u32 stamp = 0;
-      double* scan = scan_all + warp * 32;
-      int* prov = prov_all + warp * 32;
-      for (;;) {
-        int hidx = 0;
-        if (lane == 0) hidx = atomicAdd(&S.next_light, 1);
-        hidx = __shfl_sync(0xFFFFFFFFu, hidx, 0);
-        if (hidx >= nh) break;
-        const int i = all ? hidx : (int)heavy[hidx];
-        if (++stamp == 0x10000u) {  // stamp wrap: clear this warp's array
-          for (u32 q = lane; q < k; q += 32) dense[q] = 0;
+      // (3) warp phase: resumed / deep elements (or every element after an overflow)
+      const bool all = S.resume_ovf != 0;
+      const int nr = all ? n : min(S.n_resume, RCAP);
+      if (tid == 0) S.grab = 0;
+      __syncthreads();
+      if (nr > 0) {
+        for (;;) {
+          int q = 0;
+          if (lane == 0) q = atomicAdd(&S.grab, 1);
+          q = __shfl_sync(FULL, q, 0);
+          if (q >= nr) break;
+          if (++stamp > 0xFFFFu) {  // wrap: clear this warp's dense array
+            for (u32 i = lane; i < k; i += 32) dense[i] = 0;
+            __syncwarp();
+            stamp = stamp_lo;
+          }
+          u32 elem, z0 = 0, nl = 0;
+          double b0 = 0.0;
+          if (all) {
+            elem = (u32)q;
+          } else {
+            elem = rec[q].elem;
+            z0 = rec[q].z;
+            nl = rec[q].nl;
+            b0 = rec[q].b;
+          }
+          for (u32 e = lane; e < nl; e += 32) {
+            const u32 ent = rmaps[(size_t)q * CAP + e];
+            dense[ent >> 16] = (stamp << 16) | (ent & 0xFFFFu);
+          }
           __syncwarp();
-          stamp = 1;
+          u32 em = 0;
+          walk_warp<true>(load_id(ids, lo + elem), load_w(wts, lo + elem), tau, k, useed, pseed, dense,
+                          stamp, scan, prov, regs, &S.unset, em, z0, b0);
+          if (lane == 0) emitted += em;
         }
-        u32 em = 0;
-        walk_warp<true>(load_id(ids, lo + i), load_w(wts, lo + i), tau, k, useed, pseed, dense,
-                        stamp, scan, prov, regs, &S.unset, em);
-        if (lane == 0) emitted += em;
-      }
-      if (!dense_in_smem) {
-        // global dense arrays must not carry stamps into the next pass
-        __syncwarp();
-        for (u32 q = lane; q < k; q += 32) dense[q] = 0;
       }
       __syncthreads();
       if (S.unset == 0) break;
       __syncthreads();
     }
 
-    // emitted count + outputs
     if (emitted_out) {
       unsigned long long e = emitted;
 #pragma unroll
-      for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xFFFFFFFFu, e, o);
+      for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
       if (lane == 0) atomicAdd(&S.emitted, e);
     }
     __syncthreads();

@@ -100,16 +100,19 @@ __device__ __forceinline__ u32 dget(const u32* dense, u32 pos, u32 stamp) {
   return (e >> 16) == stamp ? (e & 0xFFFFu) + 1 : pos + 1;
 }
 
+// Resumes at (z_start accepted arrivals, b_start = time of the last one);
+// the caller has loaded the live permutation entries into `dense`.
 template <bool kSharedRegs>
 __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u64 useed,
                                           u64 pseed, u32* dense, u32 stamp, double* scan,
-                                          int* prov, Reg* regs, int* unset_ctr, u32& emitted) {
+                                          int* prov, Reg* regs, int* unset_ctr, u32& emitted,
+                                          u32 z_start = 0, double b_start = 0.0) {
   const unsigned FULL = 0xFFFFFFFFu;
   const int lane = threadIdx.x & 31;
   const u64 ubase = useed + id * K_ELEM;
   const u64 pbase = pseed + id * K_ELEM;
-  double b = 0.0;
-  u32 z0 = 0;
+  double b = b_start;
+  u32 z0 = z_start;
   while (z0 < k) {
     const u32 z = z0 + lane + 1;
     const bool valid = z <= k;
@@ -118,12 +121,20 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
     prov[lane] = -1;
     __syncwarp();
     if (lane == 0) {  // left-to-right prefix, the reference's summation order
+      double2* s2 = reinterpret_cast<double2*>(scan);
+      double2 v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = s2[i];
       double acc = b;
-#pragma unroll 8
-      for (int i = 0; i < 32; ++i) {
-        acc = __dadd_rn(acc, scan[i]);
-        scan[i] = acc;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        acc = __dadd_rn(acc, v[i].x);
+        v[i].x = acc;
+        acc = __dadd_rn(acc, v[i].y);
+        v[i].y = acc;
       }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) s2[i] = v[i];
     }
     __syncwarp();
     const double t = scan[lane];
@@ -167,6 +178,81 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
     __syncwarp();
   }
   __syncwarp();
+}
+
+// ---- flattened lane walker ------------------------------------------------
+// One step per call, so a warp's lanes advance different elements in
+// lock-step and a lane that finishes refills at once (no reconvergence at
+// the end of each element's queue).  The next spacing is computed before
+// the permutation step so the two dependency chains overlap (ILP).
+struct LaneWalk {
+  u64 id, ubase, pbase;
+  double w, b, t;  // b: last accepted arrival; t: pending arrival z+1
+  u32 z;           // accepted arrivals
+  int nl;          // live map entries
+};
+
+__device__ __forceinline__ void lane_start(LaneWalk& L, u64 id, double w, u32 k, u64 useed, u64 pseed) {
+  L.id = id;
+  L.w = w;
+  L.ubase = useed + id * K_ELEM;
+  L.pbase = pseed + id * K_ELEM;
+  L.b = 0.0;
+  L.z = 0;
+  L.nl = 0;
+  L.t = __dadd_rn(0.0, spacing(L.ubase, 1, w, k));
+}
+
+// Accept the pending arrival (caller checked t <= tau and nl < cap) and
+// compute the next pending one (+inf once the queue is exhausted).
+template <bool kSharedRegs>
+__device__ __forceinline__ void lane_accept(LaneWalk& L, u32 k, u32* map, int stride, Reg* regs,
+                                            int* unset_ctr) {
+  const u32 z = L.z + 1;
+  const double t = L.t;
+  const double tn = z < k ? __dadd_rn(t, spacing(L.ubase, z + 1, L.w, k))
+                          : __longlong_as_double(0x7FF0000000000000ll);
+  const u32 j = perm_draw(L.pbase, z, k);
+  const u32 zi = z - 1, ji = j - 1;
+  u32 vz = zi + 1, vj = ji + 1;
+  int sz = -1, sj = -1;
+  const int nl = L.nl;
+  for (int e = 0; e < nl; ++e) {
+    const u32 ent = map[e * stride];
+    const u32 p = ent >> 16;
+    if (p == zi) {
+      vz = (ent & 0xFFFFu) + 1;
+      sz = e;
+    }
+    if (p == ji) {
+      vj = (ent & 0xFFFFu) + 1;
+      sj = e;
+    }
+  }
+  int n2 = nl;
+  if (ji != zi) {
+    const u32 nent = (ji << 16) | (vz - 1);
+    if (sj >= 0) {
+      map[sj * stride] = nent;
+      if (sz >= 0) {
+        --n2;
+        if (sz != n2) map[sz * stride] = map[n2 * stride];
+      }
+    } else if (sz >= 0) {
+      map[sz * stride] = nent;
+    } else {
+      map[n2 * stride] = nent;
+      ++n2;
+    }
+  } else if (sz >= 0) {
+    --n2;
+    if (sz != n2) map[sz * stride] = map[n2 * stride];
+  }
+  L.nl = n2;
+  if (reg_min<kSharedRegs>(&regs[vj - 1], (u64)__double_as_longlong(t), L.id)) atomicSub(unset_ctr, 1);
+  L.b = t;
+  L.z = z;
+  L.t = tn;
 }
 
 }  // namespace gmk
