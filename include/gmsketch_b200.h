@@ -58,6 +58,9 @@ extern "C" {
 
 /* Library version (major*10000 + minor*100 + patch). */
 int gm_version(void);
+/* Debug builds (-DGM_DEBUG): first device bounds-check failure
+ * ((line << 32) | code), else 0. */
+int gm_debug_error(unsigned long long *out);
 /* Thread-local message of the last failing call ("" if none). */
 const char *gm_last_error(void);
 /* Returns and clears the data error latched on `stream` by GM_FLAG_ASYNC

@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgmsketch_b200.so")
+LIB_PATH = os.environ.get("GM_LIB_PATH") or os.path.join(_HERE, "libgmsketch_b200.so")
 
 GM_OK = 0
 GM_ERR_EMPTY_VECTOR = 1
@@ -34,6 +34,7 @@ _u64, _i64, _i32, _u32, _int, _vp, _dbl = (ctypes.c_uint64, ctypes.c_int64, ctyp
                                            ctypes.c_double)
 SIGNATURES = {
     "gm_version": (_int, []),
+    "gm_debug_error": (_int, [_vp]),
     "gm_last_error": (ctypes.c_char_p, []),
     "gm_stream_status": (_int, [_vp]),
     "gm_sketch_csr": (_int, [_vp, _int, _vp, _int, _vp, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),

@@ -32,8 +32,10 @@ int fail(int code, const char* fmt, ...) {
 #define CK(call)                                                                      \
   do {                                                                                \
     cudaError_t e_ = (call);                                                          \
-    if (e_ != cudaSuccess)                                                            \
+    if (e_ != cudaSuccess) {                                                          \
+      (void)cudaGetLastError(); /* do not leave a non-sticky error for other libs */  \
       return fail(GM_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));       \
+    }                                                                                 \
   } while (0)
 
 struct Workspace {
@@ -156,10 +158,13 @@ int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n
       int dev = 0, optin = 0;
       CK(cudaGetDevice(&dev));
       CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-      if (smem <= (size_t)optin) {
+      cudaFuncAttributes fa;
+      CK(cudaFuncGetAttributes(&fa, kern));
+      const int dyn_max = optin - (int)fa.sharedSizeBytes;
+      if (smem <= (size_t)dyn_max) {
         // one limit per function (the device maximum), so launches with a
         // smaller k never lower it under a larger k's requirement
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
       }
       it = cache.emplace(key, per_sm).first;
@@ -261,6 +266,16 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
 extern "C" {
 
 int gm_version(void) { return 100; }
+
+int gm_debug_error(unsigned long long* out) {
+#ifdef GM_DEBUG
+  CK(cudaMemcpyFromSymbol(out, g_dbg_err, sizeof(unsigned long long)));
+  return GM_OK;
+#else
+  *out = 0;
+  return GM_OK;
+#endif
+}
 
 const char* gm_last_error(void) { return g_msg; }
 

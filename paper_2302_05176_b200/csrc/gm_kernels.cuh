@@ -115,8 +115,9 @@ __global__ void __launch_bounds__(NT, 3)
   // warp stamps: >= 0x8000 so stale lane-map words (pos < 0x8000) never match
   const u32 stamp_lo = dense_smem ? 0x8000u : 1u;
   u32 stamp = stamp_lo - 1;
-  if (!dense_smem)
-    for (u32 i = lane; i < k; i += 32) dense[i] = 0;
+  // shared memory starts with whatever the previous kernel left: clear the
+  // warp's dense array once so no stale word can carry a live stamp
+  for (u32 i = lane; i < k; i += 32) dense[i] = 0;
   double* scan = scan_all + warp * 32;
   int* prov = prov_all + warp * 32;
   u32* mymap = pool + tid;
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(NT, 3)
         const double w = load_w(wts, lo + i);
         if (w >= deep_w) {
           const int r = atomicAdd(&S.n_resume, 1);
-          if (r < RCAP) {
+          if (r < RCAP && GM_OKIF(r >= 0, 25u)) {
             rec[r].elem = (u32)i;
             rec[r].z = 0;
             rec[r].nl = 0;
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(NT, 3)
           }
         } else if (w >= lpt_w) {
           const int h = atomicAdd(&S.n_heavy, 1);
-          if (h < HCAP) heavy[h] = (u32)i;
+          if (h < HCAP && GM_OKIF(h >= 0, 26u)) heavy[h] = (u32)i;
           else S.heavy_ovf = 1;
         }
       }
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(NT, 3)
               const int q = atomicAdd(&S.grab, 1);
               if (q < nh) {
                 cur = (int)heavy[q];
+                GM_CHECK(cur >= 0 && cur < n, 6u);
                 break;
               }
               const int i = q - nh;
@@ -268,9 +270,10 @@ __global__ void __launch_bounds__(NT, 3)
             nl = rec[q].nl;
             b0 = rec[q].b;
           }
+          GM_CHECK(elem < (u32)n && z0 < k && nl <= (u32)CAP, 4u);
           for (u32 e = lane; e < nl; e += 32) {
             const u32 ent = rmaps[(size_t)q * CAP + e];
-            dense[ent >> 16] = (stamp << 16) | (ent & 0xFFFFu);
+            if (GM_OKIF((ent >> 16) < k, 5u)) dense[ent >> 16] = (stamp << 16) | (ent & 0xFFFFu);
           }
           __syncwarp();
           u32 em = 0;

@@ -96,6 +96,7 @@ __device__ __forceinline__ bool walk_light(u64 id, double w, double tau, u32 k, 
 // dense: k words, entry (stamp << 16) | (val - 1); other stamps read as the
 // identity.  scan: 32 doubles, prov: 32 ints (per-warp shared scratch).
 __device__ __forceinline__ u32 dget(const u32* dense, u32 pos, u32 stamp) {
+  if (!GM_OKIF(pos < 65536u, 20u)) return pos + 1;
   const u32 e = dense[pos];
   return (e >> 16) == stamp ? (e & 0xFFFFu) + 1 : pos + 1;
 }
@@ -168,8 +169,9 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
     const u32 vj = pj >= 0 ? vjp : mj;
     // positions >= z0 + n_acc stay live: last writer of each ji stores vz
     const u32 higher = same & ~((2u << lane) - 1u);
-    if (acc && higher == 0 && ji >= z0 + (u32)n_acc) dense[ji] = (stamp << 16) | (vz - 1);
-    if (acc && reg_min<kSharedRegs>(&regs[vj - 1], (u64)__double_as_longlong(t), id))
+    GM_CHECK(!acc || (vj >= 1 && vj <= k && vz >= 1 && vz <= k && ji < k), 3u);
+    if (acc && higher == 0 && ji >= z0 + (u32)n_acc && GM_OKIF(ji < k, 21u)) dense[ji] = (stamp << 16) | (vz - 1);
+    if (acc && GM_OKIF(vj >= 1 && vj <= k, 22u) && reg_min<kSharedRegs>(&regs[vj - 1], (u64)__double_as_longlong(t), id))
       atomicSub(unset_ctr, 1);
     emitted += (u32)(n_acc + (n_acc < 32 && z0 + n_acc < k ? 1 : 0));
     if (n_acc < 32) break;
@@ -217,7 +219,8 @@ __device__ __forceinline__ void lane_accept(LaneWalk& L, u32 k, u32* map, int st
   u32 vz = zi + 1, vj = ji + 1;
   int sz = -1, sj = -1;
   const int nl = L.nl;
-  for (int e = 0; e < nl; ++e) {
+  GM_CHECK(nl >= 0 && nl <= 40, 23u);
+  for (int e = 0; e < nl && e < 40; ++e) {
     const u32 ent = map[e * stride];
     const u32 p = ent >> 16;
     if (p == zi) {
@@ -230,6 +233,7 @@ __device__ __forceinline__ void lane_accept(LaneWalk& L, u32 k, u32* map, int st
     }
   }
   int n2 = nl;
+  if (!GM_OKIF(nl < 40, 24u)) return;
   if (ji != zi) {
     const u32 nent = (ji << 16) | (vz - 1);
     if (sj >= 0) {
@@ -249,6 +253,9 @@ __device__ __forceinline__ void lane_accept(LaneWalk& L, u32 k, u32* map, int st
     if (sz != n2) map[sz * stride] = map[n2 * stride];
   }
   L.nl = n2;
+  GM_CHECK(vj >= 1 && vj <= k, 1u);
+  GM_CHECK(n2 <= 40, 2u);
+  if (vj < 1 || vj > k) return;
   if (reg_min<kSharedRegs>(&regs[vj - 1], (u64)__double_as_longlong(t), L.id)) atomicSub(unset_ctr, 1);
   L.b = t;
   L.z = z;
