@@ -1,5 +1,9 @@
-"""Summarise an ncu source page (--print-source cuda,sass --csv) by CUDA source line:
-stall samples and warp instructions executed, top-N."""
+"""Summarise an ncu source page by CUDA source line: stall samples and warp
+instructions executed, top-N.
+
+  ncu -i X.ncu-rep --page source --csv --print-source cuda,sass > src.csv
+  python tools/ncu_lines.py src.csv [N]
+"""
 import csv
 import sys
 
@@ -12,26 +16,28 @@ def main(path, top=40):
     for r in rows:
         if not r:
             continue
-        if r[0] == "File Path":
+        if r[0] in ("File Path", "File Name"):
             cur_file = r[1].split("/")[-1]
             continue
         if r[0] == "Line No":
             hdr = r
             continue
-        if hdr is None or r[0] == "" or r[0] == "Function Name":
+        if hdr is None or r[0] in ("", "Function Name"):
             continue
         try:
             line = int(r[0])
         except ValueError:
             continue
-        d = dict(zip(hdr[2:], r[2:]))
+        d = dict(zip(hdr[4:], r[4:]))
+
         def num(key):
             try:
                 return float(d.get(key, "0") or 0)
             except ValueError:
                 return 0.0
-        agg.append((num("Warp Stall Sampling (All Samples)"), num("Instructions Executed"),
-                    num("Avg. Threads Executed"), cur_file, line, r[1][:90]))
+        ie = num("Instructions Executed")
+        agg.append((num("Warp Stall Sampling (All Samples)"), ie,
+                    num("Thread Instructions Executed") / ie if ie else 0.0, cur_file, line, r[1][:90]))
     tot_s = sum(a[0] for a in agg) or 1
     tot_i = sum(a[1] for a in agg) or 1
     print(f"total stall samples {tot_s:.0f}, warp instructions {tot_i:.3e}")
