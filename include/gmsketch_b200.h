@@ -149,6 +149,17 @@ int gm_perm_draw_batch(const uint64_t *perm_seeds, const uint64_t *elements,
                        const uint64_t *steps, const uint32_t *ks, int64_t n,
                        uint32_t *out, void *stream);
 
+/* Arithmetic self-checks (device).
+ * gm_arith_check: over n keyed random inputs, counts[0] = #(branch-free
+ * divide != IEEE __ddiv_rn) on the fast weight range, counts[1] = #(device
+ * log_pos more than 1 ulp from CUDA's log).  counts: 2 device u64.
+ * gm_log_batch: out[i] = device natural log of x[i] > 0 (device arrays); the
+ * log every walker uses in -log(u) (randgen.py:186, math.log in the
+ * reference).  Both synchronise `stream`. */
+int gm_arith_check(int64_t n, uint64_t seed, unsigned long long *counts,
+                   void *stream);
+int gm_log_batch(const double *x, int64_t n, double *out, void *stream);
+
 /* Diagnostics.
  * gm_probe_arrival_rate: n_threads threads each emit `iters` exact arrivals
  * (spacing + permutation draw, no pruning or registers); the measured rate

@@ -13,7 +13,7 @@
 #include <utility>
 
 #include "../../include/gmsketch_b200.h"
-#include "gm_kernels.cuh"
+#include "gm_csr.cuh"
 
 using namespace gmk;
 
@@ -134,17 +134,27 @@ int num_sms() {
   return sms;
 }
 
-size_t csr_smem_bytes(u32 k) {
-  return (size_t)k * sizeof(Reg) + csr_pool_words(k) * 4 + RCAP * sizeof(ResumeRec) + NWARP * 32 * 8 +
-         NWARP * 32 * 4 + HCAP * 4;
+using CsrDefault = CsrCfg<128, 16, 3>;
+// alternates for tuning sweeps (GM_CSR_CFG=1..3 selects one for u32 ids + f32 weights)
+using CsrAlt1 = CsrCfg<256, 8, 3>;
+using CsrAlt2 = CsrCfg<128, 8, 4>;
+using CsrAlt3 = CsrCfg<256, 16, 2>;
+
+int csr_cfg_choice() {
+  static int c = -1;
+  if (c < 0) {
+    const char* e = getenv("GM_CSR_CFG");
+    c = e ? atoi(e) : 0;
+  }
+  return c;
 }
 
-template <class IdT, class WT>
+template <class C, class IdT, class WT>
 int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k,
                u64 useed, u64 pseed, double* y, u64* s, int64_t* em, Workspace* ws,
                cudaStream_t st, int attempt0) {
-  auto kern = csr_sketch_kernel<IdT, WT>;
-  const size_t smem = csr_smem_bytes(k);
+  auto kern = csr3_kernel<C, IdT, WT>;
+  const size_t smem = csr3_smem_bytes<C>(k);
   int per_sm = 0;
   {
     // occupancy per (kernel, smem) is cached: the launch path stays a
@@ -165,7 +175,7 @@ int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n
         // one limit per function (the device maximum), so launches with a
         // smaller k never lower it under a larger k's requirement
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NT, smem));
       }
       it = cache.emplace(key, per_sm).first;
     }
@@ -175,17 +185,17 @@ int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n
   int64_t grid = (int64_t)per_sm * num_sms();
   if (grid > n_vec) grid = n_vec;
   u32* dense = nullptr;
-  if (!csr_dense_in_smem(k)) {
-    int rc = grow(&ws->dense, &ws->dense_cap, (size_t)grid * NWARP * k, st);
+  if (k > C::KMAX_REGION) {
+    int rc = grow(&ws->dense, &ws->dense_cap, (size_t)grid * C::NWARP * k, st, true);
     if (rc) return rc;
     dense = ws->dense;
   }
-  int rc = grow(&ws->resume, &ws->resume_cap, (size_t)grid * RCAP * CAP, st);
+  int rc = grow(&ws->resume, &ws->resume_cap, (size_t)grid * C::RCAP * C::SLOTS, st);
   if (rc) return rc;
   CK(cudaMemsetAsync(ws->counters, 0, sizeof(int), st));
-  kern<<<(unsigned)grid, NT, smem, st>>>((const IdT*)ids, (const WT*)w, offsets, n_vec, k, useed,
-                                         pseed, y, s, em, ws->counters, dense, ws->resume, ws->err,
-                                         attempt0);
+  kern<<<(unsigned)grid, C::NT, smem, st>>>((const IdT*)ids, (const WT*)w, offsets, n_vec, k, useed,
+                                            pseed, y, s, em, ws->counters, dense, ws->resume, ws->err,
+                                            attempt0);
   CK(cudaGetLastError());
   return GM_OK;
 }
@@ -345,13 +355,18 @@ int gm_sketch_csr(const void* ids, int id_bits, const void* w, int w_bits, const
   // exhaustive = a single pass with tau = +inf (pass_tau's last attempt)
   const int a0 = (flags & GM_FLAG_EXHAUSTIVE) ? 3 : 0;
   if (id_bits == 32 && w_bits == 32)
-    rc = launch_csr<u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
+    switch (csr_cfg_choice()) {
+      case 1: rc = launch_csr<CsrAlt1, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0); break;
+      case 2: rc = launch_csr<CsrAlt2, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0); break;
+      case 3: rc = launch_csr<CsrAlt3, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0); break;
+      default: rc = launch_csr<CsrDefault, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
+    }
   else if (id_bits == 32)
-    rc = launch_csr<u32, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
+    rc = launch_csr<CsrDefault, u32, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
   else if (w_bits == 32)
-    rc = launch_csr<u64, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
+    rc = launch_csr<CsrDefault, u64, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
   else
-    rc = launch_csr<u64, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
+    rc = launch_csr<CsrDefault, u64, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
   if (rc == -1) return csr_by_elements(ids, id_bits, w, w_bits, offsets, n_vec, k, global_seed,
                                        stream_salt, flags, y_out, s_out, emitted_out, st);
   if (rc) return rc;
@@ -507,6 +522,27 @@ int gm_perm_draw_batch(const uint64_t* perm_seeds, const uint64_t* elements, con
   (void)cudaGetLastError();
   if (n <= 0) return GM_OK;
   randint_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(perm_seeds, elements, steps, ks, n, out);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return GM_OK;
+}
+
+int gm_arith_check(int64_t n, uint64_t seed, unsigned long long* counts, void* stream) {
+  g_msg[0] = 0;
+  (void)cudaGetLastError();
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), st));
+  if (n > 0) arith_check_kernel<<<(unsigned)(num_sms() * 8), 256, 0, st>>>(n, seed, counts);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  return GM_OK;
+}
+
+int gm_log_batch(const double* x, int64_t n, double* out, void* stream) {
+  g_msg[0] = 0;
+  (void)cudaGetLastError();
+  if (n <= 0) return GM_OK;
+  log_batch_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(x, n, out);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   return GM_OK;

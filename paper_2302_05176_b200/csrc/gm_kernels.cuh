@@ -1,9 +1,7 @@
 // gm_kernels.cuh -- the FastGM kernels (sm_100a).
 //
-//   K1 csr_sketch_kernel   batch of CSR vectors, persistent CTAs, one vector
-//                          per CTA at a time, registers in shared memory
-//                          (configs 1-3; replaces sketch_fast_counted,
-//                          sketch.py:218-311, per vector).
+//   K1 csr3_kernel         batch of CSR vectors (gm_csr.cuh; configs 1-3,
+//                          replaces sketch_fast_counted, sketch.py:218-311).
 //   K2 elem_light_kernel + elem_heavy_kernel
 //                          one huge element set (a huge vector or an
 //                          (id, weight) stream), grid-stride, registers in
@@ -47,260 +45,6 @@ __device__ __forceinline__ double pass_tau(double W, u32 k, int attempt) {
   const double c = attempt == 0 ? 2.5 : attempt == 1 ? 6.0 : attempt == 2 ? 14.0 : -1.0;
   if (c < 0.0) return __longlong_as_double(0x7FF0000000000000ll);  // +inf: full queues
   return (log((double)k) + c) / W;
-}
-
-struct ResumeRec {
-  u32 elem;  // local element index
-  u32 z;     // accepted arrivals
-  u32 nl;    // live permutation entries (stored in the CTA's global slot)
-  u32 pad;
-  double b;  // time of the last accepted arrival
-};
-
-struct CsrSmem {
-  int unset;
-  int grab;
-  int n_heavy;
-  int heavy_ovf;
-  int n_resume;
-  int resume_ovf;
-  int vec;
-  int pad;
-  unsigned long long emitted;
-  double wsum[NWARP];
-};
-
-constexpr int CAP = 40;        // lane-walker permutation entries per thread
-constexpr int HCAP = 1024;     // heaviest-first list
-constexpr int RCAP = 256;      // warp-phase records
-constexpr double LPT_DEPTH = 12.0;   // expected depth that goes first
-constexpr double DEEP_DEPTH = 48.0;  // expected depth that goes straight to the warp walker
-
-__host__ __device__ constexpr size_t csr_pool_words(u32 k) {
-  return (size_t)CAP * NT;  // lane maps; the warp phase reuses it for dense arrays when they fit
-}
-__host__ __device__ constexpr bool csr_dense_in_smem(u32 k) { return (size_t)NWARP * k <= (size_t)CAP * NT; }
-
-// K1.  Dynamic shared memory layout:
-//   Reg regs[k] | u32 pool[CAP*NT] (lane maps, then per-warp dense arrays)
-//   | ResumeRec rec[RCAP] | double scan[NWARP][32] | int prov[NWARP][32] | u32 heavy[HCAP]
-// Per vector and pass: (1) classify elements by expected depth k*w*tau
-// into a heaviest-first list and a straight-to-warp list, (2) flattened
-// lane phase (one step per lane per iteration, immediate refill), (3) warp
-// phase for elements whose permutation list overflowed (resumed) or that
-// are expected to be deep, (4) unset check -> next pass with a larger tau.
-template <class IdT, class WT>
-__global__ void __launch_bounds__(NT, 3)
-    csr_sketch_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts,
-                      const int64_t* __restrict__ offsets, int64_t n_vec, u32 k, u64 useed,
-                      u64 pseed, double* __restrict__ y_out, u64* __restrict__ s_out,
-                      int64_t* __restrict__ emitted_out, int* __restrict__ vec_counter,
-                      u32* __restrict__ dense_global, u32* __restrict__ resume_global,
-                      unsigned long long* __restrict__ err, int attempt0) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ CsrSmem S;
-  const unsigned FULL = 0xFFFFFFFFu;
-  Reg* regs = reinterpret_cast<Reg*>(smem_raw);
-  u32* pool = reinterpret_cast<u32*>(smem_raw + (size_t)k * sizeof(Reg));
-  ResumeRec* rec = reinterpret_cast<ResumeRec*>(pool + csr_pool_words(k));
-  double* scan_all = reinterpret_cast<double*>(rec + RCAP);
-  int* prov_all = reinterpret_cast<int*>(scan_all + NWARP * 32);
-  u32* heavy = reinterpret_cast<u32*>(prov_all + NWARP * 32);
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool dense_smem = csr_dense_in_smem(k);
-  u32* dense = dense_smem ? pool + (size_t)warp * k
-                          : dense_global + ((size_t)blockIdx.x * NWARP + warp) * k;
-  u32* rmaps = resume_global + (size_t)blockIdx.x * RCAP * CAP;
-  // warp stamps: >= 0x8000 so stale lane-map words (pos < 0x8000) never match
-  const u32 stamp_lo = dense_smem ? 0x8000u : 1u;
-  u32 stamp = stamp_lo - 1;
-  // shared memory starts with whatever the previous kernel left: clear the
-  // warp's dense array once so no stale word can carry a live stamp
-  for (u32 i = lane; i < k; i += 32) dense[i] = 0;
-  double* scan = scan_all + warp * 32;
-  int* prov = prov_all + warp * 32;
-  u32* mymap = pool + tid;
-
-  for (;;) {
-    if (tid == 0) S.vec = atomicAdd(vec_counter, 1);
-    __syncthreads();
-    const int64_t v = S.vec;
-    if (v >= n_vec) break;
-    const int64_t lo = offsets[v], hi = offsets[v + 1];
-    const int n = (int)(hi - lo);
-
-    // total weight (only sets tau) + validation
-    double ws = 0.0;
-    for (int i = tid; i < n; i += NT) {
-      const double w = load_w(wts, lo + i);
-      if (!weight_ok(w)) raise_error(err, 2u, (u64)v);
-      ws += w;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) ws += __shfl_xor_sync(FULL, ws, o);
-    if (lane == 0) S.wsum[warp] = ws;
-    for (u32 j = tid; j < k; j += NT) {
-      regs[j].y = INF_BITS;
-      regs[j].id = NO_ID;
-    }
-    if (tid == 0) {
-      S.unset = (int)k;
-      S.emitted = 0;
-    }
-    __syncthreads();
-    double W = 0.0;
-#pragma unroll
-    for (int i = 0; i < NWARP; ++i) W += S.wsum[i];
-    if (n == 0 && tid == 0) raise_error(err, 1u, (u64)v);
-
-    u32 emitted = 0;
-    for (int attempt = attempt0; n > 0; ++attempt) {
-      const double tau = pass_tau(W, k, attempt);
-      const double kt = (double)k * tau;  // expected depth = k * w * tau
-      const double lpt_w = LPT_DEPTH / kt, deep_w = DEEP_DEPTH / kt;
-      if (tid == 0) {
-        S.grab = 0;
-        S.n_heavy = 0;
-        S.heavy_ovf = 0;
-        S.n_resume = 0;
-        S.resume_ovf = 0;
-      }
-      __syncthreads();
-      // (1) classify
-      for (int i = tid; i < n; i += NT) {
-        const double w = load_w(wts, lo + i);
-        if (w >= deep_w) {
-          const int r = atomicAdd(&S.n_resume, 1);
-          if (r < RCAP && GM_OKIF(r >= 0, 25u)) {
-            rec[r].elem = (u32)i;
-            rec[r].z = 0;
-            rec[r].nl = 0;
-            rec[r].b = 0.0;
-          } else {
-            S.resume_ovf = 1;
-          }
-        } else if (w >= lpt_w) {
-          const int h = atomicAdd(&S.n_heavy, 1);
-          if (h < HCAP && GM_OKIF(h >= 0, 26u)) heavy[h] = (u32)i;
-          else S.heavy_ovf = 1;
-        }
-      }
-      __syncthreads();
-      const int nh = min(S.n_heavy, HCAP);
-      const bool hovf = S.heavy_ovf != 0;
-      // (2) flattened lane phase
-      {
-        LaneWalk L;
-        int cur = -1;
-        bool done = false;
-        for (;;) {
-          if (cur < 0 && !done) {
-            for (;;) {
-              const int q = atomicAdd(&S.grab, 1);
-              if (q < nh) {
-                cur = (int)heavy[q];
-                GM_CHECK(cur >= 0 && cur < n, 6u);
-                break;
-              }
-              const int i = q - nh;
-              if (i >= n) {
-                done = true;
-                break;
-              }
-              const double w = load_w(wts, lo + i);
-              if (w >= deep_w || (w >= lpt_w && !hovf)) continue;  // listed elsewhere
-              cur = i;
-              break;
-            }
-            if (cur >= 0) lane_start(L, load_id(ids, lo + cur), load_w(wts, lo + cur), k, useed, pseed);
-          }
-          if (__all_sync(FULL, cur < 0)) break;
-          if (cur >= 0) {
-            if (L.t > tau) {
-              emitted += L.z + 1;
-              cur = -1;
-            } else if (L.nl == CAP) {  // list full: hand over to the warp phase
-              const int r = atomicAdd(&S.n_resume, 1);
-              if (r < RCAP) {
-                rec[r].elem = (u32)cur;
-                rec[r].z = L.z;
-                rec[r].nl = (u32)CAP;
-                rec[r].b = L.b;
-                for (int e = 0; e < CAP; ++e) rmaps[(size_t)r * CAP + e] = mymap[e * NT];
-              } else {
-                S.resume_ovf = 1;
-              }
-              emitted += L.z;
-              cur = -1;
-            } else {
-              lane_accept<true>(L, k, mymap, NT, regs, &S.unset);
-              if (L.z == k) {
-                emitted += k;
-                cur = -1;
-              }
-            }
-          }
-        }
-      }
-      __syncthreads();
-      // (3) warp phase: resumed / deep elements (or every element after an overflow)
-      const bool all = S.resume_ovf != 0;
-      const int nr = all ? n : min(S.n_resume, RCAP);
-      if (tid == 0) S.grab = 0;
-      __syncthreads();
-      if (nr > 0) {
-        for (;;) {
-          int q = 0;
-          if (lane == 0) q = atomicAdd(&S.grab, 1);
-          q = __shfl_sync(FULL, q, 0);
-          if (q >= nr) break;
-          if (++stamp > 0xFFFFu) {  // wrap: clear this warp's dense array
-            for (u32 i = lane; i < k; i += 32) dense[i] = 0;
-            __syncwarp();
-            stamp = stamp_lo;
-          }
-          u32 elem, z0 = 0, nl = 0;
-          double b0 = 0.0;
-          if (all) {
-            elem = (u32)q;
-          } else {
-            elem = rec[q].elem;
-            z0 = rec[q].z;
-            nl = rec[q].nl;
-            b0 = rec[q].b;
-          }
-          GM_CHECK(elem < (u32)n && z0 < k && nl <= (u32)CAP, 4u);
-          for (u32 e = lane; e < nl; e += 32) {
-            const u32 ent = rmaps[(size_t)q * CAP + e];
-            if (GM_OKIF((ent >> 16) < k, 5u)) dense[ent >> 16] = (stamp << 16) | (ent & 0xFFFFu);
-          }
-          __syncwarp();
-          u32 em = 0;
-          walk_warp<true>(load_id(ids, lo + elem), load_w(wts, lo + elem), tau, k, useed, pseed, dense,
-                          stamp, scan, prov, regs, &S.unset, em, z0, b0);
-          if (lane == 0) emitted += em;
-        }
-      }
-      __syncthreads();
-      if (S.unset == 0) break;
-      __syncthreads();
-    }
-
-    if (emitted_out) {
-      unsigned long long e = emitted;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
-      if (lane == 0) atomicAdd(&S.emitted, e);
-    }
-    __syncthreads();
-    for (u32 j = tid; j < k; j += NT) {
-      y_out[v * (int64_t)k + j] = __longlong_as_double((long long)regs[j].y);
-      s_out[v * (int64_t)k + j] = regs[j].id;
-    }
-    if (tid == 0 && emitted_out) emitted_out[v] = (int64_t)S.emitted;
-    __syncthreads();
-  }
 }
 
 // ---- K2: one huge element set, registers in global memory ---------------
@@ -492,6 +236,40 @@ __global__ void randint_kernel(const u64* pseeds, const u64* elems, const u64* s
                                const u32* ks, int64_t n, u32* out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = perm_draw(pseeds[i] + elems[i] * K_ELEM, (u32)steps[i], ks[i]);
+}
+
+// ---- arithmetic self-check: ddiv_fast == __ddiv_rn on the fast range, and
+// log_pos within 1 ulp of CUDA's log, over keyed random inputs ----
+__global__ void arith_check_kernel(int64_t n, u64 seed, unsigned long long* counts) {
+  unsigned long long bad_div = 0, bad_log = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const u64 a = mix64(seed + (u64)i * K_ELEM), b = mix64(a ^ K_STEP), c = mix64(b + K_RETRY);
+    const double u = u_open(a);
+    const double L = -log_pos(u);
+    // divisor: w in [2**-940, 2**900] log-uniform-ish, times an integer m <= 65536
+    const int ex = (int)(b % 1840u) - 940;
+    const double w = ldexp(1.0 + (double)(c >> 12) * 0x1p-52, ex);
+    const double D = __dmul_rn(w, (double)(1u + (u32)(c & 0xFFFFu)));
+    const double q1 = ddiv_fast(L, D), q2 = __ddiv_rn(L, D);
+    bad_div += __double_as_longlong(q1) != __double_as_longlong(q2) && !(q1 == 0.0 && q2 == 0.0);
+    const double l2 = log(u);
+    const long long dl = __double_as_longlong(-L) - __double_as_longlong(l2);
+    bad_log += (dl > 1 || dl < -1) && !(L == 0.0 && l2 == 0.0);
+  }
+  for (int o = 16; o; o >>= 1) {
+    bad_div += __shfl_xor_sync(0xFFFFFFFFu, bad_div, o);
+    bad_log += __shfl_xor_sync(0xFFFFFFFFu, bad_log, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&counts[0], bad_div);
+    atomicAdd(&counts[1], bad_log);
+  }
+}
+
+// device log of given inputs (parity tests compare it with glibc's)
+__global__ void log_batch_kernel(const double* x, int64_t n, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = log_pos(x[i]);
 }
 
 // ---- diagnostics ----

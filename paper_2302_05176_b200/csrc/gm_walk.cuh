@@ -93,21 +93,38 @@ __device__ __forceinline__ bool walk_light(u64 id, double w, double tau, u32 k, 
 }
 
 // ---- warp walker ----------------------------------------------------------
-// dense: k words, entry (stamp << 16) | (val - 1); other stamps read as the
-// identity.  scan: 32 doubles, prov: 32 ints (per-warp shared scratch).
-__device__ __forceinline__ u32 dget(const u32* dense, u32 pos, u32 stamp) {
+// Dense view of an element's permutation: k words, entry (stamp << 16) |
+// (val - 1); words with another stamp read as the identity.  The array is a
+// plain k-word slice (global scratch) or a strided region of shared memory
+// (the owning warp's lane tables, see gm_csr.cuh).
+struct DenseFlat {
+  u32* p;
+  __device__ __forceinline__ u32& operator[](u32 i) const { return p[i]; }
+};
+struct DenseStrided {  // 128-word rows, `pitch` words apart
+  u32* p;
+  u32 pitch;
+  __device__ __forceinline__ u32& operator[](u32 i) const { return p[(i >> 7) * pitch + (i & 127u)]; }
+};
+
+template <class D>
+__device__ __forceinline__ u32 dget(const D& dense, u32 pos, u32 stamp) {
   if (!GM_OKIF(pos < 65536u, 20u)) return pos + 1;
   const u32 e = dense[pos];
   return (e >> 16) == stamp ? (e & 0xFFFFu) + 1 : pos + 1;
 }
 
-// Resumes at (z_start accepted arrivals, b_start = time of the last one);
-// the caller has loaded the live permutation entries into `dense`.
-template <bool kSharedRegs>
+// One element, 32 queue steps per iteration.  Resumes at (z_start accepted
+// arrivals, b_start = time of the last one); the caller has loaded the live
+// permutation entries into `dense`.  scan: 32 doubles, prov: 32 ints (per-warp
+// shared scratch).  mtab: Barrett constants of m = k - z + 1 for z < mtab_n
+// (nullable).  unset_ctr: decremented when a register is first set (nullable).
+template <bool kSharedRegs, bool kFast = false, class D>
 __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u64 useed,
-                                          u64 pseed, u32* dense, u32 stamp, double* scan,
+                                          u64 pseed, const D& dense, u32 stamp, double* scan,
                                           int* prov, Reg* regs, int* unset_ctr, u32& emitted,
-                                          u32 z_start = 0, double b_start = 0.0) {
+                                          u32 z_start = 0, double b_start = 0.0,
+                                          const u32* mtab = nullptr, u32 mtab_n = 0) {
   const unsigned FULL = 0xFFFFFFFFu;
   const int lane = threadIdx.x & 31;
   const u64 ubase = useed + id * K_ELEM;
@@ -117,7 +134,7 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
   while (z0 < k) {
     const u32 z = z0 + lane + 1;
     const bool valid = z <= k;
-    const double d = valid ? spacing(ubase, z, w, k) : 0.0;
+    const double d = valid ? spacing_t<kFast>(ubase, z, w, k) : 0.0;
     scan[lane] = d;
     prov[lane] = -1;
     __syncwarp();
@@ -142,7 +159,8 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
     const u32 stop = __ballot_sync(FULL, !(valid && t <= tau));
     const int n_acc = stop ? __ffs(stop) - 1 : 32;
     const bool acc = lane < n_acc;
-    const u32 j = acc ? perm_draw(pbase, z, k) : 0u;
+    u32 j = 0;
+    if (acc) j = (mtab && z < mtab_n) ? perm_draw_m(pbase, z, k, mtab[z]) : perm_draw(pbase, z, k);
     const u32 zi = z - 1, ji = j - 1;
     u32 vz = acc ? dget(dense, zi, stamp) : 0u;
     const u32 mj = acc ? dget(dense, ji, stamp) : 0u;
@@ -171,7 +189,8 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
     const u32 higher = same & ~((2u << lane) - 1u);
     GM_CHECK(!acc || (vj >= 1 && vj <= k && vz >= 1 && vz <= k && ji < k), 3u);
     if (acc && higher == 0 && ji >= z0 + (u32)n_acc && GM_OKIF(ji < k, 21u)) dense[ji] = (stamp << 16) | (vz - 1);
-    if (acc && GM_OKIF(vj >= 1 && vj <= k, 22u) && reg_min<kSharedRegs>(&regs[vj - 1], (u64)__double_as_longlong(t), id))
+    if (acc && GM_OKIF(vj >= 1 && vj <= k, 22u) &&
+        reg_min<kSharedRegs>(&regs[vj - 1], (u64)__double_as_longlong(t), id) && unset_ctr)
       atomicSub(unset_ctr, 1);
     emitted += (u32)(n_acc + (n_acc < 32 && z0 + n_acc < k ? 1 : 0));
     if (n_acc < 32) break;
@@ -180,86 +199,6 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
     __syncwarp();
   }
   __syncwarp();
-}
-
-// ---- flattened lane walker ------------------------------------------------
-// One step per call, so a warp's lanes advance different elements in
-// lock-step and a lane that finishes refills at once (no reconvergence at
-// the end of each element's queue).  The next spacing is computed before
-// the permutation step so the two dependency chains overlap (ILP).
-struct LaneWalk {
-  u64 id, ubase, pbase;
-  double w, b, t;  // b: last accepted arrival; t: pending arrival z+1
-  u32 z;           // accepted arrivals
-  int nl;          // live map entries
-};
-
-__device__ __forceinline__ void lane_start(LaneWalk& L, u64 id, double w, u32 k, u64 useed, u64 pseed) {
-  L.id = id;
-  L.w = w;
-  L.ubase = useed + id * K_ELEM;
-  L.pbase = pseed + id * K_ELEM;
-  L.b = 0.0;
-  L.z = 0;
-  L.nl = 0;
-  L.t = __dadd_rn(0.0, spacing(L.ubase, 1, w, k));
-}
-
-// Accept the pending arrival (caller checked t <= tau and nl < cap) and
-// compute the next pending one (+inf once the queue is exhausted).
-template <bool kSharedRegs>
-__device__ __forceinline__ void lane_accept(LaneWalk& L, u32 k, u32* map, int stride, Reg* regs,
-                                            int* unset_ctr) {
-  const u32 z = L.z + 1;
-  const double t = L.t;
-  const double tn = z < k ? __dadd_rn(t, spacing(L.ubase, z + 1, L.w, k))
-                          : __longlong_as_double(0x7FF0000000000000ll);
-  const u32 j = perm_draw(L.pbase, z, k);
-  const u32 zi = z - 1, ji = j - 1;
-  u32 vz = zi + 1, vj = ji + 1;
-  int sz = -1, sj = -1;
-  const int nl = L.nl;
-  GM_CHECK(nl >= 0 && nl <= 40, 23u);
-  for (int e = 0; e < nl && e < 40; ++e) {
-    const u32 ent = map[e * stride];
-    const u32 p = ent >> 16;
-    if (p == zi) {
-      vz = (ent & 0xFFFFu) + 1;
-      sz = e;
-    }
-    if (p == ji) {
-      vj = (ent & 0xFFFFu) + 1;
-      sj = e;
-    }
-  }
-  int n2 = nl;
-  if (!GM_OKIF(nl < 40, 24u)) return;
-  if (ji != zi) {
-    const u32 nent = (ji << 16) | (vz - 1);
-    if (sj >= 0) {
-      map[sj * stride] = nent;
-      if (sz >= 0) {
-        --n2;
-        if (sz != n2) map[sz * stride] = map[n2 * stride];
-      }
-    } else if (sz >= 0) {
-      map[sz * stride] = nent;
-    } else {
-      map[n2 * stride] = nent;
-      ++n2;
-    }
-  } else if (sz >= 0) {
-    --n2;
-    if (sz != n2) map[sz * stride] = map[n2 * stride];
-  }
-  L.nl = n2;
-  GM_CHECK(vj >= 1 && vj <= k, 1u);
-  GM_CHECK(n2 <= 40, 2u);
-  if (vj < 1 || vj > k) return;
-  if (reg_min<kSharedRegs>(&regs[vj - 1], (u64)__double_as_longlong(t), L.id)) atomicSub(unset_ctr, 1);
-  L.b = t;
-  L.z = z;
-  L.t = tn;
 }
 
 }  // namespace gmk
