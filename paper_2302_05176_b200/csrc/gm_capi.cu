@@ -52,6 +52,12 @@ struct Workspace {
   size_t dense_cap = 0;
   u32* resume = nullptr;
   size_t resume_cap = 0;
+  u32* csr_dense = nullptr;                // CSR warp-walker dense arrays (stamped)
+  size_t csr_dense_cap = 0;
+  double* vsum = nullptr;                  // per-vector total weight (CSR prep)
+  size_t vsum_cap = 0;
+  int* vflag = nullptr;                    // per-vector flags (CSR prep)
+  size_t vflag_cap = 0;
   void* stage = nullptr;                   // device staging for *_host calls
   size_t stage_cap = 0;
 };
@@ -105,6 +111,9 @@ int map_device_error(unsigned long long e) {
       return fail(code, "EmptyVectorError: vector %llu has no positive entries", where);
     case GM_ERR_INVALID_WEIGHT:
       return fail(code, "InvalidWeightError: weight not finite, > 0 and >= 1e-300 (vector/element %llu)", where);
+    case 3:
+      return fail(GM_ERR_INVALID_PARAMETER, "InvalidParameterError: vector %llu has more than 2**24 - 4096 elements "
+                  "(sketch it with gm_sketch_elements)", where);
     default:
       return fail(code, "device error %d at %llu", code, where);
   }
@@ -134,11 +143,11 @@ int num_sms() {
   return sms;
 }
 
-using CsrDefault = CsrCfg<128, 16, 3>;
+using CsrDefault = CsrCfg<256, 8, 2, 3>;
 // alternates for tuning sweeps (GM_CSR_CFG=1..3 selects one for u32 ids + f32 weights)
-using CsrAlt1 = CsrCfg<256, 8, 3>;
-using CsrAlt2 = CsrCfg<128, 8, 4>;
-using CsrAlt3 = CsrCfg<256, 16, 2>;
+using CsrAlt1 = CsrCfg<256, 8, 1, 3>;
+using CsrAlt2 = CsrCfg<256, 16, 2, 2>;
+using CsrAlt3 = CsrCfg<384, 8, 2, 2>;
 
 int csr_cfg_choice() {
   static int c = -1;
@@ -158,7 +167,7 @@ int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n
   int per_sm = 0;
   {
     // occupancy per (kernel, smem) is cached: the launch path stays a
-    // memset + one kernel launch
+    // memset + two kernel launches
     static std::mutex mu;
     static std::map<std::pair<const void*, size_t>, int> cache;
     std::lock_guard<std::mutex> lk(mu);
@@ -183,18 +192,22 @@ int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n
   }
   if (per_sm < 1) return -1;  // registers do not fit in shared memory: caller falls back
   int64_t grid = (int64_t)per_sm * num_sms();
-  if (grid > n_vec) grid = n_vec;
-  u32* dense = nullptr;
-  if (k > C::KMAX_REGION) {
-    int rc = grow(&ws->dense, &ws->dense_cap, (size_t)grid * C::NWARP * k, st, true);
-    if (rc) return rc;
-    dense = ws->dense;
-  }
-  int rc = grow(&ws->resume, &ws->resume_cap, (size_t)grid * C::RCAP * C::SLOTS, st);
+  const int64_t need_ctas = (n_vec + C::V - 1) / C::V;
+  if (grid > need_ctas) grid = need_ctas;
+  // own scratch: the K2 heavy kernel relies on ws->dense staying zeroed
+  int rc = grow(&ws->csr_dense, &ws->csr_dense_cap, (size_t)grid * C::NWARP * k, st);
+  if (rc) return rc;
+  rc = grow(&ws->vsum, &ws->vsum_cap, (size_t)n_vec, st);
+  if (rc) return rc;
+  rc = grow(&ws->vflag, &ws->vflag_cap, (size_t)n_vec, st);
   if (rc) return rc;
   CK(cudaMemsetAsync(ws->counters, 0, sizeof(int), st));
-  kern<<<(unsigned)grid, C::NT, smem, st>>>((const IdT*)ids, (const WT*)w, offsets, n_vec, k, useed,
-                                            pseed, y, s, em, ws->counters, dense, ws->resume, ws->err,
+  const int64_t prep_blocks = std::min<int64_t>((n_vec + 7) / 8, (int64_t)num_sms() * 16);
+  csr_prep_kernel<WT><<<(unsigned)prep_blocks, 256, 0, st>>>((const WT*)w, offsets, n_vec, ws->vsum, ws->vflag,
+                                                             ws->err);
+  CK(cudaGetLastError());
+  kern<<<(unsigned)grid, C::NT, smem, st>>>((const IdT*)ids, (const WT*)w, offsets, n_vec, k, useed, pseed,
+                                            ws->vsum, ws->vflag, y, s, em, ws->counters, ws->csr_dense, ws->err,
                                             attempt0);
   CK(cudaGetLastError());
   return GM_OK;
