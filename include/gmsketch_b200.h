@@ -160,6 +160,10 @@ int gm_arith_check(int64_t n, uint64_t seed, unsigned long long *counts,
                    void *stream);
 int gm_log_batch(const double *x, int64_t n, double *out, void *stream);
 
+/* Work counters of a library built with -DGM_STATS (tools/stats.py): copies
+ * and clears 16 u64 host words; GM_ERR_INVALID_PARAMETER in normal builds. */
+int gm_stats_read(unsigned long long *out16);
+
 /* Diagnostics.
  * gm_probe_arrival_rate: n_threads threads each emit `iters` exact arrivals
  * (spacing + permutation draw, no pruning or registers); the measured rate

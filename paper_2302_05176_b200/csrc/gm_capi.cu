@@ -302,6 +302,19 @@ int gm_debug_error(unsigned long long* out) {
 
 const char* gm_last_error(void) { return g_msg; }
 
+// GM_STATS builds only (tools/stats.py): read and clear the 16 work counters
+int gm_stats_read(unsigned long long* out16) {
+#ifdef GM_STATS
+  CK(cudaMemcpyFromSymbol(out16, g_stats, sizeof(unsigned long long) * 16));
+  unsigned long long z[16] = {0};
+  CK(cudaMemcpyToSymbol(g_stats, z, sizeof(z)));
+  return GM_OK;
+#else
+  (void)out16;
+  return fail(GM_ERR_INVALID_PARAMETER, "library built without GM_STATS");
+#endif
+}
+
 int gm_stream_status(void* stream) {
   Workspace* ws = nullptr;
   int rc = get_ws((cudaStream_t)stream, &ws);

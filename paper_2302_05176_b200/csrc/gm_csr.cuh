@@ -300,31 +300,37 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   double gw = 0.0, gtau = 0.0, gb = 0.0;
   Reg* gregs = nullptr;
   u32 gz = 0, gem = 0;
-  u32 fin = 0;    // slots whose last element this group completed (leader)
+  u32 fin = 0;    // slots this warp must finalise (warp-uniform)
   u32 stamp = 0;  // dense-array stamp of this warp
-  // prefetched next element (held by the group leader)
-  int nslot = -1;
-  u64 nid = 0;
-  double nw = 0.0;
+  // element queue of the warp: a ring of 32 entries, entry e held by lane e
+  // (slot, id, weight loaded when the entry was taken from its slot)
+  int q_slot = -1;
+  u64 q_id = 0;
+  double q_w = 0.0;
+  u32 qhead = 0, qcnt = 0;  // warp-uniform
 
-  // count a finished element (group leader); n is read before the increment:
-  // once this element is counted the slot may be finalised and reloaded
-  auto complete = [&](int s, u32 e) {
-    SlotInfo& sl = S.slot[s];
-    const int n = *(volatile int*)&sl.n;
-    if (emitted_out) atomicAdd(&sl.emitted, (unsigned long long)e);
+  // count `c` finished elements of slot s (lane 0; the warp's register
+  // updates are fenced first).  n is read before the increment: once they are
+  // counted the slot may be finalised and reloaded by another warp.
+  auto complete_batch = [&](int s, int c, unsigned long long em_sum) {
     __threadfence_block();
-    const int old = atomicAdd(&sl.done, 1);
-    if (old + 1 == n) fin |= 1u << s;
+    __syncwarp();
+    if (lane == 0) {
+      SlotInfo& sl = S.slot[s];
+      const int n = *(volatile int*)&sl.n;
+      if (emitted_out) atomicAdd(&sl.emitted, em_sum);
+      __threadfence_block();
+      const int old = atomicAdd(&sl.done, c);
+      if (old + c == n) fin |= 1u << s;
+    }
+    fin = __shfl_sync(FULL, fin, 0);
   };
 
   for (;;) {
-    // ---- (1) finalise slots whose last element this warp completed
-    unsigned wfin = __reduce_or_sync(FULL, fin);
-    fin = 0;
-    while (wfin) {
-      const int s = __ffs(wfin) - 1;
-      wfin &= wfin - 1;
+    // ---- (1) finalise slots whose last elements this warp completed
+    while (fin) {
+      const int s = __ffs(fin) - 1;
+      fin &= fin - 1;
       SlotInfo& sl = S.slot[s];
       __threadfence_block();
       Reg* regs = slot_regs<C>(smem_raw, s, k);
@@ -360,6 +366,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       const u32 z0 = wres ? __shfl_sync(FULL, gz, src) : 0u;
       const double b0 = wres ? __shfl_sync(FULL, gb, src) : 0.0;
       const bool wfast = __shfl_sync(FULL, (int)gfast, src) != 0;
+      const u32 em0 = __shfl_sync(FULL, gem, src);
       if (++stamp > 0xFFFFu) {
         for (u32 i = lane; i < k; i += 32) dense[i] = 0;
         __syncwarp();
@@ -382,20 +389,71 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         walk_warp<true, false>(wid, ww, tau, k, useed, pseed, dense, stamp, scan, prov, regs, nullptr, wem, z0, b0,
                                mtab, (u32)C::MTAB);
       wem = __shfl_sync(FULL, wem, 0);
-      if (lane == src) complete(s, gem + wem);
+      GM_STAT(3, lane == 0);  // warp walks
+      GM_STAT(4, lane == 0 ? wem : 0u);
+      complete_batch(s, 1, (unsigned long long)(em0 + wem));
       if (gbase == src) {
         gdeep = false;
         gres = false;
       }
     }
 
-    // ---- (3) groups without an element start the prefetched one
+    // ---- (3) refill the warp's element queue from the oldest open slot
+    if (qcnt < (u32)(2 * C::NGW)) {
+      int first = 0;
+      if (lane == 0) {
+        unsigned best = *(volatile unsigned*)&S.slot[0].seq;
+#pragma unroll
+        for (int i = 1; i < V; ++i) {
+          const unsigned q = *(volatile unsigned*)&S.slot[i].seq;
+          if (q < best) {
+            best = q;
+            first = i;
+          }
+        }
+      }
+      first = __shfl_sync(FULL, first, 0);
+#pragma unroll
+      for (int oi = 0; oi < V; ++oi) {
+        const u32 room = 32u - qcnt;
+        if (room == 0) break;
+        const int s = (first + oi) % V;
+        SlotInfo& sl = S.slot[s];
+        unsigned long long base = 0;
+        long long lo = 0;
+        if (lane == 0) {
+          const unsigned long long g0 = *(volatile unsigned long long*)&sl.grab;
+          if ((u32)g0 < (u32)(g0 >> 32)) {
+            base = atomicAdd(&sl.grab, (unsigned long long)room);
+            __threadfence_block();
+            lo = *(volatile long long*)&sl.lo;
+          }
+        }
+        base = __shfl_sync(FULL, base, 0);
+        const u32 n = (u32)(base >> 32), i0 = (u32)base;
+        if (i0 >= n) continue;
+        lo = __shfl_sync(FULL, lo, 0);
+        const u32 got = min(room, n - i0);
+        const u32 t = (u32)(lane - (int)((qhead + qcnt) & 31u)) & 31u;  // this lane's offset in the new run
+        if (t < got) {
+          q_slot = s;
+          q_id = (u64)__ldg(&ids[lo + i0 + t]);
+          q_w = (double)__ldg(&wts[lo + i0 + t]);
+        }
+        qcnt += got;
+      }
+    }
+
+    // ---- (4) groups without an element take the next queue entries
     {
-      const bool need = !glive && !gdeep;
-      const int ps = __shfl_sync(FULL, nslot, gbase);
-      const u64 pid = __shfl_sync(FULL, nid, gbase);
-      const double pw = __shfl_sync(FULL, nw, gbase);
-      if (need && ps >= 0) {
+      const unsigned needm = __ballot_sync(FULL, leader && !glive && !gdeep);
+      const u32 take = min((u32)__popc(needm), qcnt);
+      const u32 rho = __popc(needm & ((1u << gbase) - 1u));  // this group's rank among takers
+      const int src = (int)((qhead + rho) & 31u);
+      const int ps = __shfl_sync(FULL, q_slot, src);
+      const u64 pid = __shfl_sync(FULL, q_id, src);
+      const double pw = __shfl_sync(FULL, q_w, src);
+      if (((needm >> gbase) & 1u) && rho < take) {
         SlotInfo& sl = S.slot[ps];
         gslot = ps;
         gid = pid;
@@ -415,71 +473,27 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
           for (int b = gi; b < C::NB; b += G) *reinterpret_cast<uint4*>(gtab + b * 4) = make_uint4(0, 0, 0, 0);
           glive = true;
         }
-        if (leader) nslot = -1;
       }
-    }
-    // ---- (4) group leaders without a prefetched element take one
-    {
-      unsigned want = __ballot_sync(FULL, leader && nslot < 0);
-      if (want) {
-        int first = 0;
-        if (lane == 0) {
-          unsigned best = *(volatile unsigned*)&S.slot[0].seq;
-#pragma unroll
-          for (int i = 1; i < V; ++i) {
-            const unsigned q = *(volatile unsigned*)&S.slot[i].seq;
-            if (q < best) {
-              best = q;
-              first = i;
-            }
-          }
-        }
-        first = __shfl_sync(FULL, first, 0);
-#pragma unroll
-        for (int oi = 0; oi < V; ++oi) {
-          if (!want) break;
-          const int s = (first + oi) % V;
-          SlotInfo& sl = S.slot[s];
-          const int wl = __ffs(want) - 1;
-          unsigned long long base = 0;
-          long long lo = 0;
-          if (lane == wl) {
-            const unsigned long long g0 = *(volatile unsigned long long*)&sl.grab;
-            if ((u32)g0 < (u32)(g0 >> 32)) {
-              base = atomicAdd(&sl.grab, (unsigned long long)__popc(want));
-              __threadfence_block();
-              lo = *(volatile long long*)&sl.lo;
-            }
-          }
-          base = __shfl_sync(FULL, base, wl);
-          const u32 n = (u32)(base >> 32);
-          if ((u32)base >= n) continue;
-          lo = __shfl_sync(FULL, lo, wl);
-          if (want & (1u << lane)) {
-            const u32 idx = (u32)base + __popc(want & ((1u << lane) - 1u));
-            if (idx < n) {
-              nslot = s;
-              nid = (u64)__ldg(&ids[lo + idx]);
-              nw = (double)__ldg(&wts[lo + idx]);
-            }
-          }
-          want = __ballot_sync(FULL, leader && nslot < 0);
-        }
-      }
+      qhead = (qhead + take) & 31u;
+      qcnt -= take;
     }
 
+    GM_STAT(7, lane == 0);  // loop iterations
     // ---- exit / idle
-    const bool busy = glive || gdeep || nslot >= 0;
-    if (!__any_sync(FULL, busy)) {
-      bool open = false;
+    if (!__any_sync(FULL, glive)) {
+      if (!__any_sync(FULL, gdeep) && qcnt == 0) {
+        bool open = false;
 #pragma unroll
-      for (int s = 0; s < V; ++s) open |= *(volatile int*)&S.slot[s].state != SLOT_EMPTY;
-      if (!__shfl_sync(FULL, (int)open, 0)) break;
-      __nanosleep(200);
+        for (int s = 0; s < V; ++s) open |= *(volatile int*)&S.slot[s].state != SLOT_EMPTY;
+        if (!__shfl_sync(FULL, (int)open, 0)) break;
+        __nanosleep(200);
+      }
+      GM_STAT(0, lane == 0);
       continue;
     }
-    if (!__any_sync(FULL, glive)) continue;
     __syncwarp();  // table clears of starting groups before their probes
+    GM_STAT(1, lane == 0);          // rounds
+    GM_STAT(2, leader && glive);    // live groups summed over rounds
 
     // ---- (5) one round of every live group (uniform instruction stream)
     // table full soon: hand the element to the warp walker before the round
@@ -488,6 +502,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       gdeep = true;
       gres = true;
     }
+    bool gdone = false;
     {
       const u32 zs = gz + 1 + gi;
       const bool valid = glive && zs <= k;
@@ -545,6 +560,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       }
       if (ji == zi) vj = vz;
       const bool live = (u32)gi < nacc;
+      GM_STAT(5, live);     // accepted lane-steps
+      GM_STAT(6, valid);    // valid lane-steps computed
       int ins = 0;
       if (live && !sup && ji >= gz + nacc) ins = tab_write<C>(gtab, ji, vz);
       if (live) reg_min<true>(&gregs[vj - 1], (u64)__double_as_longlong(t), gid);
@@ -554,12 +571,27 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       if (glive) {
         if (nacc > 0) gb = tl;
         gz += nacc;
+        gem += nacc;
         if (nacc < (u32)G || gz >= k) {
-          gem += nacc + (gz < k ? 1 : 0);
+          gem += gz < k ? 1 : 0;
           glive = false;
-          if (leader) complete(gslot, gem);
-        } else {
-          gem += nacc;
+          gdone = true;
+        }
+      }
+    }
+    // ---- (6) count finished elements per slot
+    {
+      const unsigned dmask = __ballot_sync(FULL, leader && gdone);
+      if (dmask) {
+#pragma unroll
+        for (int s = 0; s < V; ++s) {
+          const bool mine = leader && gdone && gslot == s;
+          const int c = __popc(__ballot_sync(FULL, mine));
+          if (c) {
+            const unsigned long long es =
+                emitted_out ? (unsigned long long)__reduce_add_sync(FULL, mine ? gem : 0u) : 0ull;
+            complete_batch(s, c, es);
+          }
         }
       }
     }

@@ -1,0 +1,43 @@
+"""Work counters of the CSR kernel (a -DGM_STATS build of the library).
+
+  python tools/stats.py [config]      builds paper_2302_05176_b200/libgmsketch_b200_stats.so
+                                      (if missing) and runs one config-2 batch through it."""
+import ctypes
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SO = os.path.join(ROOT, "paper_2302_05176_b200", "libgmsketch_b200_stats.so")
+sys.path.insert(0, ROOT)
+if "--build" in sys.argv or not os.path.exists(SO):
+    from paper_2302_05176_b200 import build as b  # noqa: E402
+    cmd = ["nvcc", *b.NVCC_FLAGS, "-DGM_STATS", "-o", SO, *b.SOURCES, "-lcudart"]
+    subprocess.run(cmd, check=True, capture_output=True)
+    if "--build" in sys.argv:
+        sys.exit(0)
+os.environ["GM_LIB_PATH"] = SO
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2302_05176_b200 as gm  # noqa: E402
+from paper_2302_05176_b200 import _lib, workloads  # noqa: E402
+
+L = _lib.load()
+ids, w, off, k, seed = workloads.config2()
+d_ids = torch.from_numpy(ids.view(np.int32)).cuda()
+d_w = torch.from_numpy(w).cuda()
+d_off = torch.from_numpy(off).cuda()
+gm.sketch_csr(d_ids, d_w, d_off, k, gm.SeedScheme(seed))
+torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * 16)()
+L.gm_stats_read(buf)
+gm.sketch_csr(d_ids, d_w, d_off, k, gm.SeedScheme(seed))
+torch.cuda.synchronize()
+L.gm_stats_read(buf)
+names = ["idle iters", "rounds", "live group-rounds", "warp walks", "warp-walk arrivals", "accepted lane-steps",
+         "valid lane-steps", "loop iterations"]
+for i, nme in enumerate(names):
+    print(f"{nme:22s} {buf[i]:>14,d}")
+print(f"lanes per round live: {buf[2] / max(buf[1], 1):.2f} groups of 8; accepted/valid {buf[5] / max(buf[6], 1):.3f}")
