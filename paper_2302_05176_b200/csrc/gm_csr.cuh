@@ -6,60 +6,51 @@
 // randgen.py:158-207) is folded into the k registers; a pass that leaves a
 // register unset is repeated with a larger tau.
 //
-// Group walker.  An element is owned by a group of G lanes that advances its
-// queue G steps per round: lane i of the group computes step z+1+i -- the
-// spacing -log(u)/(w(k-z'+1)), the permutation draw j and the probes of the
-// element's Fisher-Yates table -- all lanes in parallel; then
-//   * the arrival times are summed left to right in the reference's order
-//     (randgen.py:186) by a G-1 step shuffle chain,
-//   * the first arrival beyond tau ends the element (steps after it are
-//     discarded, exactly as the reference's queue stops there),
-//   * the swaps of the round are resolved inside the group in step order
-//     (the value an earlier step moved to a position provides later reads),
-//   * surviving positions are written back to the table and every accepted
-//     arrival is folded into its register (128-bit CAS lexicographic min).
-// Every lane of the warp runs the same instruction stream (groups differ
-// only in data), the exact sum order costs G-1 shuffles, and an element in
-// flight needs one table per G lanes.
+// Lane walker: one lane walks one element, one queue step per loop
+// iteration (straight-line step: the next spacing, the permutation draw,
+// both table probes, the register read; rare cases take a slow path).  A lane
+// whose element ends takes the next one from its warp's element queue (32
+// entries with ids and weights already loaded, refilled 32 at a time), so
+// lanes never wait for the longest queue of their warp.  An element whose
+// expected depth k*w*tau is large, or whose lane table fills up, is walked by
+// the whole warp in-line (walk_warp, 32 steps per iteration), the other lanes
+// pausing their own elements.
 //
 // Pipelined CTA (no CTA-wide barrier after the prologue): the CTA keeps V
 // vectors in flight ("slots": k registers in shared memory + a header);
-// groups take elements from the oldest slot that still has some, so a
-// vector's tail overlaps its successor.  An element whose expected depth
-// k*w*tau is large, or whose table fills up, is walked by the whole warp
-// in-line (walk_warp, 32 steps per iteration).  The group that completes a
-// slot's last element has its warp finalise the slot: check every register
-// is set (else reopen it for the next pass), write the sketch out, load the
-// next vector.
+// warps take elements from the oldest slot that still has some, so a
+// vector's tail overlaps its successor.  Finished elements are counted per
+// warp and slot; the warp that counts a slot's last element finalises it:
+// check every register is set (else reopen it for the next pass with a
+// larger tau), write the sketch out, load the next vector.
 //
-// Group table (LazyPermutation, randgen.py:146-155): NB buckets of 4 words,
-// open addressing with bucket-linear probing, cleared when the group takes
-// an element; a word is (position << 16) | (value - 1), 0 = empty (a stored
-// position is some j - 1 >= z >= 1).  Entries are never removed (an entry
-// below the current step is dead and never looked up again).
+// Lane permutation table (LazyPermutation, randgen.py:146-155): NB buckets of
+// 4 words per lane, open addressing with bucket-linear probing, cleared when
+// the lane takes an element; a word is (position << 16) | (value - 1), 0 =
+// empty (a stored position is some j - 1 >= z >= 1).  Entries are never
+// removed (an entry below the current step is dead and never looked up
+// again).  Layout is bucket-major ((bucket * NT + lane) * 4 + way) so a
+// warp's LDS.128 touch distinct bank quads per quarter-warp.
 #pragma once
 
 #include "gm_kernels.cuh"
 
 namespace gmk {
 
-template <int NT_, int NB_, int G_ = 4, int V_ = 2, int MINB_ = 1>
+template <int NT_, int NB_, int V_ = 2, int MINB_ = 1>
 struct CsrCfg {
   static constexpr int NT = NT_;               // threads per CTA
   static constexpr int NWARP = NT_ / 32;
   static constexpr int MINB = MINB_;           // __launch_bounds__ min blocks
-  static constexpr int G = G_;                 // lanes per element
-  static constexpr int NGW = 32 / G_;          // groups per warp
-  static constexpr int NB = NB_;               // buckets per group table (power of 2)
-  static constexpr int SLOTS = 4 * NB_;        // words per group table
+  static constexpr int NB = NB_;               // buckets per lane table (power of 2)
+  static constexpr int SLOTS = 4 * NB_;        // words per lane table
   static constexpr int CAPI = SLOTS * 13 / 16; // inserts per element before hand-over
   static constexpr int V = V_;                 // vectors in flight per CTA
   static constexpr int MTAB = 256;             // Barrett table entries (z < MTAB)
   static constexpr int NMAX = (1 << 24) - 4096;  // elements per vector
   // expected depth at which an element goes straight to the warp walker
-  static constexpr double kDeep = CAPI * 0.6;
+  static constexpr double kDeep = CAPI * 0.62;
   static_assert((NB_ & (NB_ - 1)) == 0, "NB must be a power of two");
-  static_assert(G_ == 2 || G_ == 4 || G_ == 8, "G in {2, 4, 8}");
   static_assert(V_ >= 1 && V_ <= 4, "1..4 slots");
 };
 
@@ -89,70 +80,133 @@ struct CsrShared {
 
 template <class C>
 __host__ __device__ constexpr size_t csr3_smem_bytes(u32 k) {
-  return (size_t)C::V * k * sizeof(Reg)                 // registers of the slots
-         + (size_t)(C::NT / C::G) * C::SLOTS * 4       // group tables
-         + (size_t)C::MTAB * 4                         // Barrett table
-         + (size_t)C::NWARP * 32 * (8 + 4);            // warp-walker scan + prov
+  return (size_t)C::V * k * sizeof(Reg)               // registers of the slots
+         + (size_t)C::NT * C::SLOTS * 4              // lane tables
+         + (size_t)C::MTAB * 4                       // Barrett table
+         + (size_t)C::NWARP * 32 * (8 + 4);          // warp-walker scan + prov
 }
 
-// ---- group table -----------------------------------------------------------
+// ---- lane table ----------------------------------------------------------
+template <class C>
 __device__ __forceinline__ uint4 tab_bucket(const u32* tab, u32 b) {
-  return *reinterpret_cast<const uint4*>(tab + b * 4);
+  return *reinterpret_cast<const uint4*>(tab + b * (C::NT * 4));
 }
 
 // Fast probe of one bucket for position p (p >= 1, or p = 0 whose identity
 // value 1 an empty word also yields): xor with p << 16 leaves the matching
 // word (at most one) below 2**16 with low half = value - 1.  Returns the min
-// over the 4 words (< 2**16 iff found).  Ways fill in order, so a bucket
-// with a zero last word has a free way and ends the probe sequence.
+// over the 4 words (< 2**16 iff found).  Ways fill in order, so a bucket is
+// full iff its last word is non-zero and the first empty way is the number
+// of non-zero words among the first three.
 __device__ __forceinline__ u32 probe_min(const uint4 q, u32 p) {
   const u32 k16 = p << 16;
   return min(min(q.x ^ k16, q.y ^ k16), min(q.z ^ k16, q.w ^ k16));
 }
+__device__ __forceinline__ u32 first_empty(const uint4 q) { return q.z ? 3u : q.y ? 2u : q.x ? 1u : 0u; }
 
-// Full lookup (slow path): value at position p, identity if absent.
+// Full lookup (slow path): value at position p (identity if absent) | word
+// index of its entry << 16 (0x3FFF if absent) | first empty word on the
+// probe path << 30 (0x3FFF if none).
 template <class C>
-__device__ __noinline__ u32 tab_value(const u32* tab, u32 p) {
-  u32 b = p & (C::NB - 1);
+__device__ __noinline__ u64 tab_find(const u32* tab, u32 p) {
+  u32 val = p + 1, slot = 0x3FFFu, fre = 0x3FFFu, b = p & (C::NB - 1);
   for (int it = 0; it < C::NB; ++it) {
-    const uint4 q = tab_bucket(tab, b);
-    const u32 mm = probe_min(q, p);
-    if (mm < 0x10000u) return (mm & 0xFFFFu) + 1;
-    if (q.w == 0u) break;
+    const uint4 q = tab_bucket<C>(tab, b);
+    const u32 e[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int wy = 3; wy >= 0; --wy) {
+      if ((e[wy] >> 16) == p && e[wy] != 0u) {
+        slot = b * 4 + wy;
+        val = (e[wy] & 0xFFFFu) + 1;
+      }
+      if (e[wy] == 0u) fre = b * 4 + wy;
+    }
+    if (slot != 0x3FFFu || fre != 0x3FFFu) break;
     b = (b + 1) & (C::NB - 1);
   }
-  return p + 1;
+  return (u64)val | ((u64)slot << 16) | ((u64)fre << 30);
 }
 
-// Write (p -> val) into the table: overwrite p's word or claim the first
-// empty word on p's probe path (CAS: other lanes of the group insert in the
-// same round).  Returns 1 if a new word was used, 0 if p was overwritten,
-// -1 if the table is full.
 template <class C>
-__device__ __forceinline__ int tab_write(u32* tab, u32 p, u32 val) {
-  const u32 e = (p << 16) | (val - 1);
-  u32 b = p & (C::NB - 1);
-  for (int it = 0; it < C::NB; ++it) {
-    uint4 q = tab_bucket(tab, b);
-    for (;;) {
-      const u32 w4[4] = {q.x, q.y, q.z, q.w};
-      int hit = -1, fre = -1;
+__device__ __forceinline__ void tab_put(u32* tab, u32 slot, u32 e) {
+  tab[(slot >> 2) * (C::NT * 4) + (slot & 3)] = e;
+}
+
+template <class C>
+__device__ __forceinline__ void tab_clear(u32* tab) {
 #pragma unroll
-      for (int wy = 3; wy >= 0; --wy) {
-        if (w4[wy] != 0u && (w4[wy] >> 16) == p) hit = wy;
-        if (w4[wy] == 0u) fre = wy;
-      }
-      if (hit >= 0) {
-        tab[b * 4 + hit] = e;
-        return 0;
-      }
-      if (fre < 0) break;  // bucket full: next bucket
-      if (atomicCAS(&tab[b * 4 + fre], 0u, e) == 0u) return 1;
-      q = tab_bucket(tab, b);  // lost the word to another lane: re-read
-    }
-    b = (b + 1) & (C::NB - 1);
+  for (int b = 0; b < C::NB; ++b) *reinterpret_cast<uint4*>(tab + b * (C::NT * 4)) = make_uint4(0, 0, 0, 0);
+}
+
+// ---- lane walker state -----------------------------------------------------
+struct Lane {
+  u64 id, ubase, pbase;
+  double w, b, t, tau;
+  Reg* regs;
+  u32 z;
+  int used;
+  int slot;
+  bool fast;
+};
+
+// One accepted queue step of the lane's element (or, when fresh, only the
+// first arrival).  Returns 0: continue, 1: element finished (first arrival
+// beyond tau or queue exhausted), 2: table full (state before the step kept
+// for a warp to resume).
+template <class C>
+__device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const u32* mtab, u32 k) {
+  const bool acc = !fresh;
+  const u32 zs = L.z + 1;
+  // permutation draw of step zs and both first-bucket probes
+  const u64 g = mix64(L.pbase + (u64)zs * K_STEP);
+  const u32 m = k - zs + 1, M = mtab[min(zs, (u32)C::MTAB - 1)];
+  u32 r = mod_barrett((u32)(g >> 32), m, M);
+  r = mod_barrett((r << 16) | ((u32)g >> 16), m, M);
+  r = mod_barrett((r << 16) | ((u32)g & 0xFFFFu), m, M);
+  u32 ji = zs - 1 + r;
+  const u32 zi = zs - 1;
+  const u32 bj = ji & (C::NB - 1);
+  const uint4 qz = tab_bucket<C>(mytab, zi & (C::NB - 1)), qj = tab_bucket<C>(mytab, bj);
+  const u32 mz = probe_min(qz, zi), mj = probe_min(qj, ji);
+  // next arrival's spacing (independent of this step's permutation work)
+  const u32 zn = acc ? min(zs + 1, k) : 1u;
+  const u64 x = mix64(L.ubase + (u64)zn * K_STEP);
+  const double Lg = -log_pos(u_open(x));
+  const double D = __dmul_rn(L.w, (double)(k - zn + 1));
+  double dq = ddiv_fast(Lg, D);
+  // fast case: no draw rejection, zi resolved in its first bucket, ji absent
+  // from the table with a free way in its first bucket
+  const bool slow = acc & (((u32)(g >> 32) == 0xFFFFFFFFu) | (zs >= (u32)C::MTAB) |
+                           ((mz >= 0x10000u) & (qz.w != 0u)) | (mj < 0x10000u) | (qj.w != 0u));
+  u32 vz = mz < 0x10000u ? (mz & 0xFFFFu) + 1 : zi + 1;
+  u32 vj = ji + 1;
+  u32 put_slot = bj * 4 + first_empty(qj);
+  bool fresh_slot = true;
+  if (!L.fast) dq = __ddiv_rn(Lg, D);
+  if (slow) {
+    ji = perm_draw(L.pbase, zs, k) - 1;
+    vz = (u32)tab_find<C>(mytab, zi) & 0xFFFFu;
+    const u64 fj = tab_find<C>(mytab, ji);
+    vj = (u32)fj & 0xFFFFu;
+    const u32 sj = (u32)(fj >> 16) & 0x3FFFu, fr = (u32)(fj >> 30) & 0x3FFFu;
+    fresh_slot = sj == 0x3FFFu;
+    put_slot = fresh_slot ? fr : sj;
   }
-  return -1;
+  if (acc) {
+    if (ji == zi) {
+      vj = vz;
+    } else if (!fresh_slot || (L.used < C::CAPI && put_slot != 0x3FFFu)) {
+      tab_put<C>(mytab, put_slot, (ji << 16) | (vz - 1));
+      L.used += fresh_slot;
+    } else {
+      return 2;
+    }
+    reg_min<true>(&L.regs[vj - 1], (u64)__double_as_longlong(L.t), L.id);
+    L.b = L.t;
+    L.z = zs;
+  }
+  L.t = __dadd_rn(L.b, dq);
+  return (L.z >= k || L.t > L.tau) ? 1 : 0;
 }
 
 // ---- vector slots ----------------------------------------------------------
@@ -254,7 +308,7 @@ __global__ void __launch_bounds__(256) csr_prep_kernel(const WT* __restrict__ wt
 }
 
 // ---- K1 ---------------------------------------------------------------------
-// Dynamic shared memory: Reg regs[V][k] | u32 tables[NT/G][SLOTS] | u32 mtab[MTAB]
+// Dynamic shared memory: Reg regs[V][k] | u32 tables[NB][NT][4] | u32 mtab[MTAB]
 //   | double scan[NWARP][32] | int prov[NWARP][32]
 template <class C, class IdT, class WT>
 __global__ void __launch_bounds__(C::NT, C::MINB)
@@ -264,23 +318,22 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
                 double* __restrict__ y_out, u64* __restrict__ s_out,
                 int64_t* __restrict__ emitted_out, int* __restrict__ vec_counter,
                 u32* __restrict__ dense_global, unsigned long long* __restrict__ err, int attempt0) {
-  constexpr int NT = C::NT, NWARP = C::NWARP, V = C::V, G = C::G;
-  constexpr unsigned GMASK = (1u << G) - 1u;
+  constexpr int NT = C::NT, NWARP = C::NWARP, V = C::V;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ CsrShared S;
   const unsigned FULL = 0xFFFFFFFFu;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gi = lane & (G - 1), gbase = lane & ~(G - 1);  // rank in group, group's first lane
-  const bool leader = gi == 0;
+  const unsigned lt_mask = (1u << lane) - 1u;
 
   u32* tables = reinterpret_cast<u32*>(smem_raw + (size_t)V * k * sizeof(Reg));
-  u32* mtab = tables + (size_t)(NT / G) * C::SLOTS;
+  u32* mtab = tables + (size_t)NT * C::SLOTS;
   double* scan = reinterpret_cast<double*>(mtab + C::MTAB) + warp * 32;
   int* prov = reinterpret_cast<int*>(reinterpret_cast<double*>(mtab + C::MTAB) + NWARP * 32) + warp * 32;
-  u32* gtab = tables + (size_t)(tid / G) * C::SLOTS;  // this lane's group table
+  u32* mytab = tables + tid * 4;
   u32* dense = dense_global + ((size_t)blockIdx.x * NWARP + warp) * k;
 
   for (u32 z = tid; z < (u32)C::MTAB; z += NT) mtab[z] = (z >= 1 && z <= k) ? barrett_magic(k - z + 1) : 0u;
+  tab_clear<C>(mytab);
   for (u32 i = lane; i < k; i += 32) dense[i] = 0;  // stamps restart every launch
   if (tid < V) {
     S.slot[tid].state = SLOT_EMPTY;
@@ -293,13 +346,16 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   if (warp < V) slot_load<C>(S, warp, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane);
   __syncthreads();
 
-  // group state (identical in the G lanes of a group)
-  bool glive = false, gdeep = false, gres = false, gfast = true;
-  int gslot = 0, gused = 0;
-  u64 gid = 0, gub = 0, gpb = 0;
-  double gw = 0.0, gtau = 0.0, gb = 0.0;
-  Reg* gregs = nullptr;
-  u32 gz = 0, gem = 0;
+  Lane L;
+  L.z = 0;
+  L.used = 0;
+  L.slot = 0;
+  L.b = L.t = L.tau = L.w = 0.0;
+  L.id = L.ubase = L.pbase = 0;
+  L.regs = nullptr;
+  L.fast = true;
+  bool live = false, fresh = false, deep = false, resume = false;
+  u32 em = 0;     // arrivals computed for the current element
   u32 fin = 0;    // slots this warp must finalise (warp-uniform)
   u32 stamp = 0;  // dense-array stamp of this warp
   // element queue of the warp: a ring of 32 entries, entry e held by lane e
@@ -327,7 +383,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   };
 
   for (;;) {
-    // ---- (1) finalise slots whose last elements this warp completed
+    // ---- (1) finalise slots whose last elements this warp counted
     while (fin) {
       const int s = __ffs(fin) - 1;
       fin &= fin - 1;
@@ -354,28 +410,28 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     }
 
     // ---- (2) warp walks: deep elements and resumed (table-full) elements
-    unsigned dm = __ballot_sync(FULL, leader && gdeep);
+    unsigned dm = __ballot_sync(FULL, deep);
     while (dm) {
       const int src = __ffs(dm) - 1;
       dm &= dm - 1;
-      const int s = __shfl_sync(FULL, gslot, src);
-      const u64 wid = __shfl_sync(FULL, gid, src);
-      const double ww = __shfl_sync(FULL, gw, src);
-      const double tau = __shfl_sync(FULL, gtau, src);
-      const bool wres = __shfl_sync(FULL, (int)gres, src) != 0;
-      const u32 z0 = wres ? __shfl_sync(FULL, gz, src) : 0u;
-      const double b0 = wres ? __shfl_sync(FULL, gb, src) : 0.0;
-      const bool wfast = __shfl_sync(FULL, (int)gfast, src) != 0;
-      const u32 em0 = __shfl_sync(FULL, gem, src);
+      const int s = __shfl_sync(FULL, L.slot, src);
+      const u64 wid = __shfl_sync(FULL, L.id, src);
+      const double ww = __shfl_sync(FULL, L.w, src);
+      const double tau = __shfl_sync(FULL, L.tau, src);
+      const bool wres = __shfl_sync(FULL, (int)resume, src) != 0;
+      const u32 z0 = wres ? __shfl_sync(FULL, L.z, src) : 0u;
+      const double b0 = wres ? __shfl_sync(FULL, L.b, src) : 0.0;
+      const bool wfast = __shfl_sync(FULL, (int)L.fast, src) != 0;
+      const u32 em0 = __shfl_sync(FULL, em, src);
       if (++stamp > 0xFFFFu) {
         for (u32 i = lane; i < k; i += 32) dense[i] = 0;
         __syncwarp();
         stamp = 1;
       }
-      if (wres) {  // the group's live table entries -> dense array
-        const u32* stab = tables + (size_t)(warp * C::NGW + src / G) * C::SLOTS;
+      if (wres) {  // the source lane's live table entries -> dense array
+        const u32* stab = tables + (warp * 32 + src) * 4;
         for (u32 wi = lane; wi < (u32)C::SLOTS; wi += 32) {
-          const u32 e = stab[wi];
+          const u32 e = stab[(wi >> 2) * (NT * 4) + (wi & 3)];
           if (e != 0u && (e >> 16) >= z0) dense[e >> 16] = (stamp << 16) | (e & 0xFFFFu);
         }
         __syncwarp();
@@ -392,14 +448,14 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       GM_STAT(3, lane == 0);  // warp walks
       GM_STAT(4, lane == 0 ? wem : 0u);
       complete_batch(s, 1, (unsigned long long)(em0 + wem));
-      if (gbase == src) {
-        gdeep = false;
-        gres = false;
+      if (lane == src) {
+        deep = false;
+        resume = false;
       }
     }
 
     // ---- (3) refill the warp's element queue from the oldest open slot
-    if (qcnt < (u32)(2 * C::NGW)) {
+    if (qcnt < 16u) {
       int first = 0;
       if (lane == 0) {
         unsigned best = *(volatile unsigned*)&S.slot[0].seq;
@@ -444,44 +500,47 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       }
     }
 
-    // ---- (4) groups without an element take the next queue entries
+    // ---- (4) lanes without an element take the next queue entries
     {
-      const unsigned needm = __ballot_sync(FULL, leader && !glive && !gdeep);
+      const unsigned needm = __ballot_sync(FULL, !live && !deep);
       const u32 take = min((u32)__popc(needm), qcnt);
-      const u32 rho = __popc(needm & ((1u << gbase) - 1u));  // this group's rank among takers
-      const int src = (int)((qhead + rho) & 31u);
-      const int ps = __shfl_sync(FULL, q_slot, src);
-      const u64 pid = __shfl_sync(FULL, q_id, src);
-      const double pw = __shfl_sync(FULL, q_w, src);
-      if (((needm >> gbase) & 1u) && rho < take) {
-        SlotInfo& sl = S.slot[ps];
-        gslot = ps;
-        gid = pid;
-        gw = pw;
-        gtau = sl.tau;
-        gfast = sl.fast != 0;
-        gregs = slot_regs<C>(smem_raw, ps, k);
-        gub = useed + pid * K_ELEM;
-        gpb = pseed + pid * K_ELEM;
-        gb = 0.0;
-        gz = 0;
-        gused = 0;
-        gem = 0;
-        if (pw >= sl.deep_w) {
-          gdeep = true;
-        } else {
-          for (int b = gi; b < C::NB; b += G) *reinterpret_cast<uint4*>(gtab + b * 4) = make_uint4(0, 0, 0, 0);
-          glive = true;
+      if (take) {
+        const u32 rho = __popc(needm & lt_mask);
+        const int src = (int)((qhead + rho) & 31u);
+        const int ps = __shfl_sync(FULL, q_slot, src);
+        const u64 pid = __shfl_sync(FULL, q_id, src);
+        const double pw = __shfl_sync(FULL, q_w, src);
+        if (((needm >> lane) & 1u) && rho < take) {
+          SlotInfo& sl = S.slot[ps];
+          L.slot = ps;
+          L.id = pid;
+          L.w = pw;
+          L.tau = sl.tau;
+          L.fast = sl.fast != 0;
+          L.regs = slot_regs<C>(smem_raw, ps, k);
+          L.ubase = useed + pid * K_ELEM;
+          L.pbase = pseed + pid * K_ELEM;
+          L.b = 0.0;
+          L.z = 0;
+          L.used = 0;
+          em = 0;
+          if (pw >= sl.deep_w) {
+            deep = true;
+          } else {
+            tab_clear<C>(mytab);
+            live = true;
+            fresh = true;
+          }
         }
+        qhead = (qhead + take) & 31u;
+        qcnt -= take;
       }
-      qhead = (qhead + take) & 31u;
-      qcnt -= take;
     }
 
     GM_STAT(7, lane == 0);  // loop iterations
     // ---- exit / idle
-    if (!__any_sync(FULL, glive)) {
-      if (!__any_sync(FULL, gdeep) && qcnt == 0) {
+    if (!__any_sync(FULL, live)) {
+      if (!__any_sync(FULL, deep) && qcnt == 0) {
         bool open = false;
 #pragma unroll
         for (int s = 0; s < V; ++s) open |= *(volatile int*)&S.slot[s].state != SLOT_EMPTY;
@@ -491,107 +550,35 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       GM_STAT(0, lane == 0);
       continue;
     }
-    __syncwarp();  // table clears of starting groups before their probes
-    GM_STAT(1, lane == 0);          // rounds
-    GM_STAT(2, leader && glive);    // live groups summed over rounds
+    GM_STAT(1, lane == 0);  // lane-step iterations
+    GM_STAT(2, live);       // live lanes summed over them
 
-    // ---- (5) one round of every live group (uniform instruction stream)
-    // table full soon: hand the element to the warp walker before the round
-    if (glive && gused > C::CAPI - G) {
-      glive = false;
-      gdeep = true;
-      gres = true;
-    }
-    bool gdone = false;
-    {
-      const u32 zs = gz + 1 + gi;
-      const bool valid = glive && zs <= k;
-      const u32 zc = min(zs, k);
-      // permutation draw of step zc and the pre-round table probes
-      const u64 g = mix64(gpb + (u64)zc * K_STEP);
-      const u32 m = k - zc + 1, M = mtab[min(zc, (u32)C::MTAB - 1)];
-      u32 r = mod_barrett((u32)(g >> 32), m, M);
-      r = mod_barrett((r << 16) | ((u32)g >> 16), m, M);
-      r = mod_barrett((r << 16) | ((u32)g & 0xFFFFu), m, M);
-      u32 ji = zc - 1 + r;
-      const u32 zi = zc - 1;
-      const uint4 qz = tab_bucket(gtab, zi & (C::NB - 1)), qj = tab_bucket(gtab, ji & (C::NB - 1));
-      const u32 mz = probe_min(qz, zi), mj = probe_min(qj, ji);
-      // spacing of step zc
-      const u64 x = mix64(gub + (u64)zc * K_STEP);
-      const double Lg = -log_pos(u_open(x));
-      const double D = __dmul_rn(gw, (double)(k - zc + 1));
-      double sp = ddiv_fast(Lg, D);
-      const bool slow = valid & (((u32)(g >> 32) == 0xFFFFFFFFu) | (zc >= (u32)C::MTAB) |
-                                 ((mz >= 0x10000u) & (qz.w != 0u)) | ((mj >= 0x10000u) & (qj.w != 0u)));
-      u32 vz = mz < 0x10000u ? (mz & 0xFFFFu) + 1 : zi + 1;
-      u32 vj = mj < 0x10000u ? (mj & 0xFFFFu) + 1 : ji + 1;
-      if (!gfast) sp = __ddiv_rn(Lg, D);
-      if (slow) {
-        ji = perm_draw(gpb, zc, k) - 1;
-        vz = tab_value<C>(gtab, zi);
-        vj = tab_value<C>(gtab, ji);
-      }
-      // arrival times, summed left to right in step order (randgen.py:186)
-      double t = __dadd_rn(gb, sp);
-#pragma unroll
-      for (int q = 1; q < G; ++q) {
-        const double p = __shfl_up_sync(FULL, t, 1);
-        if (gi == q) t = __dadd_rn(p, sp);
-      }
-      const bool acc = valid && t <= gtau;
-      const unsigned am = (__ballot_sync(FULL, acc) >> gbase) & GMASK;
-      const u32 nacc = (u32)__ffs(~am) - 1;  // accepted prefix of the round
-      // swaps of the round in step order: a later step reads what an earlier
-      // one moved; `sup`: a later accepted step rewrites the same position
-      bool sup = false;
-#pragma unroll
-      for (int q = 0; q < G; ++q) {
-        const u32 jq = __shfl_sync(FULL, ji, gbase + q);
-        const u32 vq = __shfl_sync(FULL, vz, gbase + q);
-        if ((u32)q < nacc) {
-          if (gi > q) {
-            if (jq == zi) vz = vq;
-            if (jq == ji) vj = vq;
-          } else if (gi < q && jq == ji) {
-            sup = true;
-          }
-        }
-      }
-      if (ji == zi) vj = vz;
-      const bool live = (u32)gi < nacc;
-      GM_STAT(5, live);     // accepted lane-steps
-      GM_STAT(6, valid);    // valid lane-steps computed
-      int ins = 0;
-      if (live && !sup && ji >= gz + nacc) ins = tab_write<C>(gtab, ji, vz);
-      if (live) reg_min<true>(&gregs[vj - 1], (u64)__double_as_longlong(t), gid);
-      gused += __popc((__ballot_sync(FULL, ins == 1) >> gbase) & GMASK);
-      const double tl = __shfl_sync(FULL, t, gbase + (nacc > 0 ? nacc - 1 : 0));
-      __syncwarp();
-      if (glive) {
-        if (nacc > 0) gb = tl;
-        gz += nacc;
-        gem += nacc;
-        if (nacc < (u32)G || gz >= k) {
-          gem += gz < k ? 1 : 0;
-          glive = false;
-          gdone = true;
-        }
+    // ---- (5) one lane step
+    bool done = false;
+    if (live) {
+      const int rc = lane_step<C>(L, fresh, mytab, mtab, k);
+      fresh = false;
+      if (rc == 1) {
+        em += L.z < k ? L.z + 1 : L.z;
+        live = false;
+        done = true;
+      } else if (rc == 2) {
+        em += L.z;
+        live = false;
+        deep = true;
+        resume = true;
       }
     }
     // ---- (6) count finished elements per slot
-    {
-      const unsigned dmask = __ballot_sync(FULL, leader && gdone);
-      if (dmask) {
+    if (__any_sync(FULL, done)) {
 #pragma unroll
-        for (int s = 0; s < V; ++s) {
-          const bool mine = leader && gdone && gslot == s;
-          const int c = __popc(__ballot_sync(FULL, mine));
-          if (c) {
-            const unsigned long long es =
-                emitted_out ? (unsigned long long)__reduce_add_sync(FULL, mine ? gem : 0u) : 0ull;
-            complete_batch(s, c, es);
-          }
+      for (int s = 0; s < V; ++s) {
+        const bool mine = done && L.slot == s;
+        const int c = __popc(__ballot_sync(FULL, mine));
+        if (c) {
+          const unsigned long long es =
+              emitted_out ? (unsigned long long)__reduce_add_sync(FULL, mine ? em : 0u) : 0ull;
+          complete_batch(s, c, es);
         }
       }
     }

@@ -36,7 +36,7 @@ L.gm_stats_read(buf)
 gm.sketch_csr(d_ids, d_w, d_off, k, gm.SeedScheme(seed))
 torch.cuda.synchronize()
 L.gm_stats_read(buf)
-names = ["idle iters", "rounds", "live group-rounds", "warp walks", "warp-walk arrivals", "accepted lane-steps",
+names = ["idle iters", "step iters", "live lane-steps", "warp walks", "warp-walk arrivals", "accepted lane-steps",
          "valid lane-steps", "loop iterations"]
 for i, nme in enumerate(names):
     print(f"{nme:22s} {buf[i]:>14,d}")
