@@ -46,6 +46,7 @@ struct CsrCfg {
   static constexpr int SLOTS = 4 * NB_;        // words per lane table
   static constexpr int CAPI = SLOTS * 13 / 16; // inserts per element before hand-over
   static constexpr int V = V_;                 // vectors in flight per CTA
+  static constexpr int U = 4;                  // lane steps per loop iteration
   static constexpr int MTAB = 256;             // Barrett table entries (z < MTAB)
   static constexpr int NMAX = (1 << 24) - 4096;  // elements per vector
   // expected depth at which an element goes straight to the warp walker
@@ -174,14 +175,19 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
   const double Lg = -log_pos(u_open(x));
   const double D = __dmul_rn(L.w, (double)(k - zn + 1));
   double dq = ddiv_fast(Lg, D);
-  // fast case: no draw rejection, zi resolved in its first bucket, ji absent
-  // from the table with a free way in its first bucket
+  // fast case: no draw rejection, zi resolved in its first bucket, ji found
+  // in its first bucket (overwrite) or absent with a free way there (insert)
+  const bool jfound = mj < 0x10000u;
   const bool slow = acc & (((u32)(g >> 32) == 0xFFFFFFFFu) | (zs >= (u32)C::MTAB) |
-                           ((mz >= 0x10000u) & (qz.w != 0u)) | (mj < 0x10000u) | (qj.w != 0u));
+                           ((mz >= 0x10000u) & (qz.w != 0u)) | (!jfound & (qj.w != 0u)));
   u32 vz = mz < 0x10000u ? (mz & 0xFFFFu) + 1 : zi + 1;
-  u32 vj = ji + 1;
-  u32 put_slot = bj * 4 + first_empty(qj);
-  bool fresh_slot = true;
+  u32 vj = jfound ? (mj & 0xFFFFu) + 1 : ji + 1;
+  const u32 k16 = ji << 16;
+  const u32 jway = jfound ? (((qj.x ^ k16) < 0x10000u) ? 0u : ((qj.y ^ k16) < 0x10000u) ? 1u
+                                                           : ((qj.z ^ k16) < 0x10000u) ? 2u : 3u)
+                          : first_empty(qj);
+  u32 put_slot = bj * 4 + jway;
+  bool fresh_slot = !jfound;
   if (!L.fast) dq = __ddiv_rn(Lg, D);
   if (slow) {
     ji = perm_draw(L.pbase, zs, k) - 1;
@@ -553,20 +559,23 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     GM_STAT(1, lane == 0);  // lane-step iterations
     GM_STAT(2, live);       // live lanes summed over them
 
-    // ---- (5) one lane step
+    // ---- (5) C::U lane steps (a lane whose element ends idles for the rest)
     bool done = false;
-    if (live) {
-      const int rc = lane_step<C>(L, fresh, mytab, mtab, k);
-      fresh = false;
-      if (rc == 1) {
-        em += L.z < k ? L.z + 1 : L.z;
-        live = false;
-        done = true;
-      } else if (rc == 2) {
-        em += L.z;
-        live = false;
-        deep = true;
-        resume = true;
+#pragma unroll 1
+    for (int u = 0; u < C::U; ++u) {
+      if (live) {
+        const int rc = lane_step<C>(L, fresh, mytab, mtab, k);
+        fresh = false;
+        if (rc == 1) {
+          em += L.z < k ? L.z + 1 : L.z;
+          live = false;
+          done = true;
+        } else if (rc == 2) {
+          em += L.z;
+          live = false;
+          deep = true;
+          resume = true;
+        }
       }
     }
     // ---- (6) count finished elements per slot
