@@ -148,7 +148,31 @@ struct Lane {
   int used;
   int slot;
   bool fast;
+  // register update in flight: a 128-bit CAS issued in one step and checked
+  // in the next, so its ~220-cycle round trip overlaps the next step's work
+  Reg* pr;           // register (nullptr: none pending)
+  u64 pcy, pcid;     // value the CAS expected
+  u64 pny, pnid;     // value it installs
+  u64 poy, poid;     // value it found
 };
+
+// finish the pending register update: a CAS that found another value (a
+// concurrent update) is retried while (t, id) is still lexicographically less
+__device__ __forceinline__ void lane_settle(Lane& L) {
+  if (L.pr) {
+    u64 oy = L.poy, oid = L.poid;
+    if (oy != L.pcy || oid != L.pcid) {
+      while (lex_less(L.pny, L.pnid, oy, oid)) {
+        u64 ry, rid;
+        cas128_shared(L.pr, oy, oid, L.pny, L.pnid, ry, rid);
+        if (ry == oy && rid == oid) break;
+        oy = ry;
+        oid = rid;
+      }
+    }
+    L.pr = nullptr;
+  }
+}
 
 // One accepted queue step of the lane's element (or, when fresh, only the
 // first arrival).  Returns 0: continue, 1: element finished (first arrival
@@ -205,14 +229,35 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
       tab_put<C>(mytab, put_slot, (ji << 16) | (vz - 1));
       L.used += fresh_slot;
     } else {
+      lane_settle(L);
       return 2;
     }
+#ifdef GM_DEFER_CAS
+    // the previous step's CAS has had this step's work to complete
+    lane_settle(L);
+    Reg* r = &L.regs[vj - 1];
+    const u64 ty = (u64)__double_as_longlong(L.t);
+    u64 cy, cid;
+    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
+                 : "=l"(cy), "=l"(cid) : "r"((u32)__cvta_generic_to_shared(r)) : "memory");
+    if (lex_less(ty, L.id, cy, cid)) {
+      cas128_shared(r, cy, cid, ty, L.id, L.poy, L.poid);
+      L.pr = r;
+      L.pcy = cy;
+      L.pcid = cid;
+      L.pny = ty;
+      L.pnid = L.id;
+    }
+#else
     reg_min<true>(&L.regs[vj - 1], (u64)__double_as_longlong(L.t), L.id);
+#endif
     L.b = L.t;
     L.z = zs;
   }
   L.t = __dadd_rn(L.b, dq);
-  return (L.z >= k || L.t > L.tau) ? 1 : 0;
+  const int rc = (L.z >= k || L.t > L.tau) ? 1 : 0;
+  if (rc) lane_settle(L);  // the element is counted as finished after this call
+  return rc;
 }
 
 // ---- vector slots ----------------------------------------------------------
@@ -360,16 +405,21 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   L.id = L.ubase = L.pbase = 0;
   L.regs = nullptr;
   L.fast = true;
+  L.pr = nullptr;
   bool live = false, fresh = false, deep = false, resume = false;
   u32 em = 0;     // arrivals computed for the current element
   u32 fin = 0;    // slots this warp must finalise (warp-uniform)
   u32 stamp = 0;  // dense-array stamp of this warp
   // element queue of the warp: a ring of 32 entries, entry e held by lane e
   // (slot, id, weight loaded when the entry was taken from its slot)
-  int q_slot = -1;
-  u64 q_id = 0;
-  double q_w = 0.0;
-  u32 qhead = 0, qcnt = 0;  // warp-uniform
+  // Two sets of 32 entries (entry e held by lane e): one is consumed while
+  // the other is refilled, so the shuffles that hand out entries never read a
+  // register whose global load is still in flight.
+  int qa_slot = -1, qb_slot = -1;
+  u64 qa_id = 0, qb_id = 0;
+  double qa_w = 0.0, qb_w = 0.0;
+  u32 qcur = 0, qhead = 0, qcnt = 0;  // warp-uniform: current set, its head and count
+  u32 qnext = 0;                      // entries loaded into the other set
 
   // count `c` finished elements of slot s (lane 0; the warp's register
   // updates are fenced first).  n is read before the increment: once they are
@@ -388,7 +438,14 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     fin = __shfl_sync(FULL, fin, 0);
   };
 
+#ifdef GM_STATS
+  long long t_prev = 0;
+  int t_sec = 15;
+#endif
   for (;;) {
+#ifdef GM_STATS
+    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 8; }
+#endif
     // ---- (1) finalise slots whose last elements this warp counted
     while (fin) {
       const int s = __ffs(fin) - 1;
@@ -415,6 +472,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       slot_load<C>(S, s, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane);
     }
 
+#ifdef GM_STATS
+    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 9; }
+#endif
     // ---- (2) warp walks: deep elements and resumed (table-full) elements
     unsigned dm = __ballot_sync(FULL, deep);
     while (dm) {
@@ -460,8 +520,11 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       }
     }
 
-    // ---- (3) refill the warp's element queue from the oldest open slot
-    if (qcnt < 16u) {
+#ifdef GM_STATS
+    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 10; }
+#endif
+    // ---- (3) refill the idle queue set from the oldest open slot
+    if (qnext == 0) {
       int first = 0;
       if (lane == 0) {
         unsigned best = *(volatile unsigned*)&S.slot[0].seq;
@@ -477,7 +540,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       first = __shfl_sync(FULL, first, 0);
 #pragma unroll
       for (int oi = 0; oi < V; ++oi) {
-        const u32 room = 32u - qcnt;
+        const u32 room = 32u - qnext;
         if (room == 0) break;
         const int s = (first + oi) % V;
         SlotInfo& sl = S.slot[s];
@@ -496,26 +559,52 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         if (i0 >= n) continue;
         lo = __shfl_sync(FULL, lo, 0);
         const u32 got = min(room, n - i0);
-        const u32 t = (u32)(lane - (int)((qhead + qcnt) & 31u)) & 31u;  // this lane's offset in the new run
+        const u32 t = (u32)lane - qnext;  // this lane's offset in the new run
         if (t < got) {
-          q_slot = s;
-          q_id = (u64)__ldg(&ids[lo + i0 + t]);
-          q_w = (double)__ldg(&wts[lo + i0 + t]);
+          const u64 id = (u64)__ldg(&ids[lo + i0 + t]);
+          const double w = (double)__ldg(&wts[lo + i0 + t]);
+          if (qcur) {
+            qa_slot = s;
+            qa_id = id;
+            qa_w = w;
+          } else {
+            qb_slot = s;
+            qb_id = id;
+            qb_w = w;
+          }
         }
-        qcnt += got;
+        qnext += got;
       }
     }
+    if (qcnt == 0 && qnext > 0) {  // current set used up: switch
+      qcur ^= 1u;
+      qhead = 0;
+      qcnt = qnext;
+      qnext = 0;
+    }
 
+#ifdef GM_STATS
+    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 11; }
+#endif
     // ---- (4) lanes without an element take the next queue entries
     {
       const unsigned needm = __ballot_sync(FULL, !live && !deep);
       const u32 take = min((u32)__popc(needm), qcnt);
       if (take) {
         const u32 rho = __popc(needm & lt_mask);
-        const int src = (int)((qhead + rho) & 31u);
-        const int ps = __shfl_sync(FULL, q_slot, src);
-        const u64 pid = __shfl_sync(FULL, q_id, src);
-        const double pw = __shfl_sync(FULL, q_w, src);
+        const int src = (int)(qhead + rho) & 31;
+        int ps;
+        u64 pid;
+        double pw;
+        if (qcur) {
+          ps = __shfl_sync(FULL, qb_slot, src);
+          pid = __shfl_sync(FULL, qb_id, src);
+          pw = __shfl_sync(FULL, qb_w, src);
+        } else {
+          ps = __shfl_sync(FULL, qa_slot, src);
+          pid = __shfl_sync(FULL, qa_id, src);
+          pw = __shfl_sync(FULL, qa_w, src);
+        }
         if (((needm >> lane) & 1u) && rho < take) {
           SlotInfo& sl = S.slot[ps];
           L.slot = ps;
@@ -538,15 +627,17 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
             fresh = true;
           }
         }
-        qhead = (qhead + take) & 31u;
+        qhead += take;
         qcnt -= take;
       }
     }
 
-    GM_STAT(7, lane == 0);  // loop iterations
+#ifdef GM_STATS
+    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 12; }
+#endif
     // ---- exit / idle
     if (!__any_sync(FULL, live)) {
-      if (!__any_sync(FULL, deep) && qcnt == 0) {
+      if (!__any_sync(FULL, deep) && qcnt == 0 && qnext == 0) {
         bool open = false;
 #pragma unroll
         for (int s = 0; s < V; ++s) open |= *(volatile int*)&S.slot[s].state != SLOT_EMPTY;
@@ -559,6 +650,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     GM_STAT(1, lane == 0);  // lane-step iterations
     GM_STAT(2, live);       // live lanes summed over them
 
+#ifdef GM_STATS
+    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 13; }
+#endif
     // ---- (5) C::U lane steps (a lane whose element ends idles for the rest)
     bool done = false;
 #pragma unroll 1
@@ -578,6 +672,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         }
       }
     }
+#ifdef GM_STATS
+    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 14; }
+#endif
     // ---- (6) count finished elements per slot
     if (__any_sync(FULL, done)) {
 #pragma unroll

@@ -40,4 +40,8 @@ names = ["idle iters", "step iters", "live lane-steps", "warp walks", "warp-walk
          "valid lane-steps", "loop iterations"]
 for i, nme in enumerate(names):
     print(f"{nme:22s} {buf[i]:>14,d}")
+sec = {8: "finalise", 9: "warp walks", 10: "refill", 11: "start", 12: "exit/idle", 13: "lane steps", 14: "completions"}  # section after each marker
+tot = sum(buf[i] for i in sec) or 1
+for i, nme in sec.items():
+    print(f"  cycles {nme:12s} {100 * buf[i] / tot:5.1f}%")
 print(f"lanes per round live: {buf[2] / max(buf[1], 1):.2f} groups of 8; accepted/valid {buf[5] / max(buf[6], 1):.3f}")
