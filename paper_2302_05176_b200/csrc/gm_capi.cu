@@ -400,6 +400,18 @@ int gm_sketch_csr(const void* ids, int id_bits, const void* w, int w_bits, const
   return check_sync(ws, st);
 }
 
+// device address of a page-locked host buffer (nullptr if the buffer is
+// pageable): the kernels can store their results straight into it
+static void* pinned_device_ptr(void* host) {
+  if (!host) return nullptr;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 int gm_sketch_csr_host(const void* ids, int id_bits, const void* w, int w_bits,
                        const int64_t* offsets, int64_t n_vec, int32_t k, uint64_t global_seed,
                        uint64_t stream_salt, uint32_t flags, double* y_out, uint64_t* s_out,
@@ -417,26 +429,35 @@ int gm_sketch_csr_host(const void* ids, int id_bits, const void* w, int w_bits,
   const int64_t n = offsets[n_vec];
   const size_t ib = (size_t)n * (id_bits / 8), wb = (size_t)n * (w_bits / 8);
   const size_t ob = (size_t)(n_vec + 1) * 8, yb = (size_t)n_vec * k * 8;
+  // results go straight to page-locked host buffers (the kernel's stores
+  // overlap its compute); pageable ones are staged on the device and copied
+  double* dy_host = (double*)pinned_device_ptr(y_out);
+  u64* ds_host = (u64*)pinned_device_ptr(s_out);
+  int64_t* dem_host = (int64_t*)pinned_device_ptr(emitted_out);
+  const bool direct = dy_host && ds_host && (!emitted_out || dem_host);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  const size_t need = al(ib) + al(wb) + al(ob) + 2 * al(yb) + al((size_t)n_vec * 8);
+  const size_t need = al(ib) + al(wb) + al(ob) + (direct ? 0 : 2 * al(yb) + al((size_t)n_vec * 8));
   rc = grow((unsigned char**)&ws->stage, &ws->stage_cap, need, st);
   if (rc) return rc;
   unsigned char* base = (unsigned char*)ws->stage;
   void* d_ids = base;
   void* d_w = base + al(ib);
   int64_t* d_off = (int64_t*)(base + al(ib) + al(wb));
-  double* d_y = (double*)((unsigned char*)d_off + al(ob));
-  u64* d_s = (u64*)((unsigned char*)d_y + al(yb));
-  int64_t* d_em = emitted_out ? (int64_t*)((unsigned char*)d_s + al(yb)) : nullptr;
-  CK(cudaMemcpyAsync(d_ids, ids, ib, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_w, w, wb, cudaMemcpyHostToDevice, st));
+  unsigned char* d_rest = (unsigned char*)d_off + al(ob);
+  double* d_y = direct ? dy_host : (double*)d_rest;
+  u64* d_s = direct ? ds_host : (u64*)(d_rest + al(yb));
+  int64_t* d_em = !emitted_out ? nullptr : direct ? dem_host : (int64_t*)(d_rest + 2 * al(yb));
   CK(cudaMemcpyAsync(d_off, offsets, ob, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_w, w, wb, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_ids, ids, ib, cudaMemcpyHostToDevice, st));
   rc = gm_sketch_csr(d_ids, id_bits, d_w, w_bits, d_off, n_vec, k, global_seed, stream_salt,
                      flags | GM_FLAG_ASYNC, d_y, d_s, d_em, stream);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(y_out, d_y, yb, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(s_out, d_s, yb, cudaMemcpyDeviceToHost, st));
-  if (d_em) CK(cudaMemcpyAsync(emitted_out, d_em, (size_t)n_vec * 8, cudaMemcpyDeviceToHost, st));
+  if (!direct) {
+    CK(cudaMemcpyAsync(y_out, d_y, yb, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(s_out, d_s, yb, cudaMemcpyDeviceToHost, st));
+    if (d_em) CK(cudaMemcpyAsync(emitted_out, d_em, (size_t)n_vec * 8, cudaMemcpyDeviceToHost, st));
+  }
   return check_sync(ws, st);
 }
 
