@@ -39,6 +39,19 @@ __device__ __forceinline__ bool weight_ok(double w) {
   return isfinite(w) && w > 0.0 && w >= 1e-300;
 }
 
+// Cheap exact pre-filter of an element's first arrival: t1 = -log(u1)/(w k)
+// exceeds tau when u1 < exp(-tau w k).  The threshold is taken in fp32 with
+// a 2**-12 relative margin (the rounded product and __expf are within ~2**-19 of
+// exp(-tau w k) for arguments below 87; beyond that __expf underflows to 0 and
+// nothing is skipped), so an element is skipped only if its exact fp64
+// arrival is beyond tau: no log, no divide, no permutation for it.
+__device__ __forceinline__ bool first_arrival_beyond(u64 ubase, double w, double tau, u32 k) {
+  const float x = (float)(tau * w * (double)k);  // fp64 product: no fp32 under/overflow of w or tau
+  const double thr = (double)__expf(-x) * (1.0 - 0x1p-12);
+  const double u1 = u_open(mix64(ubase + K_STEP));
+  return u1 < thr;
+}
+
 // threshold for pass `attempt` given total weight W (tau
 // bounds the final max register with probability 1 - e^-c)
 __device__ __forceinline__ double pass_tau(double W, u32 k, int attempt) {
@@ -63,19 +76,38 @@ __global__ void __launch_bounds__(NT)
   u32 emitted = 0;
   u32* mymap = maps + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * NT;
-  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += stride) {
-    const double w = load_w(wts, i);
-    if (!weight_ok(w)) {
-      raise_error(err, 2u, (u64)i);
-      continue;
+  // four coalesced loads in flight per thread, then the cheap first-arrival
+  // filter; the rare survivors walk their queues
+  for (int64_t i0 = (int64_t)blockIdx.x * NT + threadIdx.x; i0 < n; i0 += 4 * stride) {
+    double wv[4];
+    u64 idv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * stride;
+      wv[u] = i < n ? load_w(wts, i) : 1.0;
+      idv[u] = i < n ? load_id(ids, i) : 0;
     }
-    bool ok = false;
-    if (w < light_w)
-      ok = walk_light<false>(load_id(ids, i), w, tau, k, useed, pseed, mymap, NT, 16, regs,
-                             unset_ctr, emitted);
-    if (!ok) {
-      const unsigned long long h = atomicAdd(heavy_count, 1ull);
-      if ((int64_t)h < heavy_cap) heavy_list[h] = (u64)i;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= n) break;
+      const double w = wv[u];
+      if (!weight_ok(w)) {
+        raise_error(err, 2u, (u64)i);
+        continue;
+      }
+      const u64 id = idv[u];
+      if (first_arrival_beyond(useed + id * K_ELEM, w, tau, k)) {
+        emitted += 1;
+        continue;
+      }
+      bool ok = false;
+      if (w < light_w)
+        ok = walk_light<false>(id, w, tau, k, useed, pseed, mymap, NT, 16, regs, unset_ctr, emitted);
+      if (!ok) {
+        const unsigned long long h = atomicAdd(heavy_count, 1ull);
+        if ((int64_t)h < heavy_cap) heavy_list[h] = (u64)i;
+      }
     }
   }
   if (emitted_total) {
