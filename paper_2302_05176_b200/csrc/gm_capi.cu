@@ -143,11 +143,11 @@ int num_sms() {
   return sms;
 }
 
-using CsrDefault = CsrCfg<256, 16, 2, 2>;
+using CsrDefault = CsrCfg<256, 16, 2, 2, 75>;
 // alternates for tuning sweeps (GM_CSR_CFG=1..3 selects one for u32 ids + f32 weights)
-using CsrAlt1 = CsrCfg<256, 8, 1, 4>;
-using CsrAlt2 = CsrCfg<256, 16, 1, 3>;
-using CsrAlt3 = CsrCfg<384, 8, 2, 2>;
+using CsrAlt1 = CsrCfg<256, 16, 2, 2, 75>;
+using CsrAlt2 = CsrCfg<256, 16, 2, 2, 85>;
+using CsrAlt3 = CsrCfg<256, 16, 2, 2, 95>;
 
 int csr_cfg_choice() {
   static int c = -1;

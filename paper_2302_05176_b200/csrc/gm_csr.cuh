@@ -37,7 +37,7 @@
 
 namespace gmk {
 
-template <int NT_, int NB_, int V_ = 2, int MINB_ = 1>
+template <int NT_, int NB_, int V_ = 2, int MINB_ = 1, int DEEP_PCT_ = 62>
 struct CsrCfg {
   static constexpr int NT = NT_;               // threads per CTA
   static constexpr int NWARP = NT_ / 32;
@@ -50,7 +50,7 @@ struct CsrCfg {
   static constexpr int MTAB = 256;             // Barrett table entries (z < MTAB)
   static constexpr int NMAX = (1 << 24) - 4096;  // elements per vector
   // expected depth at which an element goes straight to the warp walker
-  static constexpr double kDeep = CAPI * 0.62;
+  static constexpr double kDeep = CAPI * (DEEP_PCT_ / 100.0);
   static_assert((NB_ & (NB_ - 1)) == 0, "NB must be a power of two");
   static_assert(V_ >= 1 && V_ <= 4, "1..4 slots");
 };
@@ -84,6 +84,7 @@ __host__ __device__ constexpr size_t csr3_smem_bytes(u32 k) {
   return (size_t)C::V * k * sizeof(Reg)               // registers of the slots
          + (size_t)C::NT * C::SLOTS * 4              // lane tables
          + (size_t)C::MTAB * 4                       // Barrett table
+         + 128 * 32                                  // log table copy
          + (size_t)C::NWARP * 32 * (8 + 4);          // warp-walker scan + prov
 }
 
@@ -154,7 +155,14 @@ struct Lane {
   u64 pcy, pcid;     // value the CAS expected
   u64 pny, pnid;     // value it installs
   u64 poy, poid;     // value it found
+  // software pipeline (lane_step_p): the draw of the step to accept (j - 1,
+  // or NEED_SLOW_DRAW) and the spacing quotient of the step after it, both
+  // computed one call ahead
+  u32 jz;
+  double dqn;
 };
+
+constexpr u32 NEED_SLOW_DRAW = 0xFFFFFFFFu;
 
 // finish the pending register update: a CAS that found another value (a
 // concurrent update) is retried while (t, id) is still lexicographically less
@@ -179,7 +187,8 @@ __device__ __forceinline__ void lane_settle(Lane& L) {
 // beyond tau or queue exhausted), 2: table full (state before the step kept
 // for a warp to resume).
 template <class C>
-__device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const u32* mtab, u32 k) {
+__device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const u32* mtab, u32 k,
+                                         const double (*ltab)[4]) {
   const bool acc = !fresh;
   const u32 zs = L.z + 1;
   // permutation draw of step zs and both first-bucket probes
@@ -196,7 +205,7 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
   // next arrival's spacing (independent of this step's permutation work)
   const u32 zn = acc ? min(zs + 1, k) : 1u;
   const u64 x = mix64(L.ubase + (u64)zn * K_STEP);
-  const double Lg = -log_pos(u_open(x));
+  const double Lg = -log_pos_t<true>(u_open(x), ltab);
   const double D = __dmul_rn(L.w, (double)(k - zn + 1));
   double dq = ddiv_fast(Lg, D);
   // fast case: no draw rejection, zi resolved in its first bucket, ji found
@@ -255,6 +264,133 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
     L.z = zs;
   }
   L.t = __dadd_rn(L.b, dq);
+  const int rc = (L.z >= k || L.t > L.tau) ? 1 : 0;
+  if (rc) lane_settle(L);  // the element is counted as finished after this call
+  return rc;
+}
+
+// One queue step zs (arrival time t) with full table lookups and the exact
+// draw: the slow path of the lane steps.  Returns false if the table is full
+// (nothing changed).
+template <class C>
+__device__ __noinline__ bool lane_step_generic(Lane& L, u32 zs, double t, u32* mytab, u32 k) {
+  const u32 ji = perm_draw(L.pbase, zs, k) - 1, zi = zs - 1;
+  const u32 vz = (u32)tab_find<C>(mytab, zi) & 0xFFFFu;
+  const u64 fj = tab_find<C>(mytab, ji);
+  u32 vj = (u32)fj & 0xFFFFu;
+  if (ji == zi) {
+    vj = vz;
+  } else {
+    const u32 sj = (u32)(fj >> 16) & 0x3FFFu, fr = (u32)(fj >> 30) & 0x3FFFu;
+    const bool fresh_slot = sj == 0x3FFFu;
+    if (fresh_slot && (L.used >= C::CAPI || fr == 0x3FFFu)) return false;
+    tab_put<C>(mytab, fresh_slot ? fr : sj, (ji << 16) | (vz - 1));
+    L.used += fresh_slot;
+  }
+  reg_min<true>(&L.regs[vj - 1], (u64)__double_as_longlong(t), L.id);
+  return true;
+}
+
+// ---- pipelined lane step --------------------------------------------------
+// j - 1 of step zs by the fast Barrett reduction, or NEED_SLOW_DRAW when the
+// rejection branch or a step beyond the Barrett table needs the exact draw
+template <class C>
+__device__ __forceinline__ u32 lane_draw(const Lane& L, u32 zs, const u32* mtab, u32 k) {
+  const u32 zc = min(zs, k);
+  const u64 g = mix64(L.pbase + (u64)zc * K_STEP);
+  const u32 m = k - zc + 1, M = mtab[min(zc, (u32)C::MTAB - 1)];
+  u32 r = mod_barrett((u32)(g >> 32), m, M);
+  r = mod_barrett((r << 16) | ((u32)g >> 16), m, M);
+  r = mod_barrett((r << 16) | ((u32)g & 0xFFFFu), m, M);
+  const bool bad = ((u32)(g >> 32) == 0xFFFFFFFFu) | (zc >= (u32)C::MTAB);
+  return bad ? NEED_SLOW_DRAW : zc - 1 + r;
+}
+
+// spacing quotient of step z (clamped to k) by the branch-free divide, and
+// its operands for the exact divide of elements outside its range
+__device__ __forceinline__ double lane_sp(const Lane& L, u32 z, u32 k, double& Lg, double& D) {
+  const u32 zc = min(z, k);
+  const u64 x = mix64(L.ubase + (u64)zc * K_STEP);
+  Lg = -log_pos(u_open(x));
+  D = __dmul_rn(L.w, (double)(k - zc + 1));
+  return ddiv_fast(Lg, D);
+}
+
+// Software-pipelined lane step.  A call accepts step zs = z + 1 (pending
+// arrival L.t) with the draw L.jz computed by the previous call, and starts
+// the draw of step zs + 1 and the spacing of step zs + 2 for the calls after
+// it; the register CAS issued here is checked by the next call.  So the only
+// chain a call waits on is probe -> resolve -> CAS issue; the long hash/log
+// chains of later steps run underneath.  Returns 0: continue, 1: element
+// finished, 2: table full (state before step zs kept for a warp to resume).
+template <class C>
+__device__ __forceinline__ int lane_step_p(Lane& L, bool fresh, u32* mytab, const u32* mtab, u32 k) {
+  if (fresh) {  // pending arrival of step 1, spacing of step 2, draw of step 1
+    double L1, D1, L2, D2;
+    double s1 = lane_sp(L, 1u, k, L1, D1);
+    double s2 = lane_sp(L, 2u, k, L2, D2);
+    L.jz = lane_draw<C>(L, 1u, mtab, k);
+    if (!L.fast) {
+      s1 = __ddiv_rn(L1, D1);
+      s2 = __ddiv_rn(L2, D2);
+    }
+    L.dqn = s2;
+    L.t = __dadd_rn(0.0, s1);
+    return L.t > L.tau ? 1 : 0;
+  }
+  lane_settle(L);  // the previous call's CAS: its result has had a call to arrive
+  const u32 zs = L.z + 1, zi = zs - 1;
+  const u32 jd = L.jz;
+  const bool rej = jd == NEED_SLOW_DRAW;
+  const u32 ji = rej ? zi : jd;
+  const u32 bj = ji & (C::NB - 1);
+  const uint4 qz = tab_bucket<C>(mytab, zi & (C::NB - 1)), qj = tab_bucket<C>(mytab, bj);
+  // next steps' chains (consumed by the next calls)
+  const u32 jn = lane_draw<C>(L, zs + 1, mtab, k);
+  double L2, D2;
+  double dq2 = lane_sp(L, zs + 2, k, L2, D2);
+  // resolve step zs from the pre-step table
+  const u32 mz = probe_min(qz, zi), mj = probe_min(qj, ji);
+  const bool jfound = mj < 0x10000u;
+  const bool slow = rej | ((mz >= 0x10000u) & (qz.w != 0u)) | (!jfound & (qj.w != 0u));
+  const u32 vz = mz < 0x10000u ? (mz & 0xFFFFu) + 1 : zi + 1;
+  u32 vj = jfound ? (mj & 0xFFFFu) + 1 : ji + 1;
+  const u32 k16 = ji << 16;
+  const u32 jway = jfound ? (((qj.x ^ k16) < 0x10000u) ? 0u : ((qj.y ^ k16) < 0x10000u) ? 1u
+                                                           : ((qj.z ^ k16) < 0x10000u) ? 2u : 3u)
+                          : first_empty(qj);
+  const bool moved = ji != zi;
+  if (!moved) vj = vz;
+  if (!slow && moved && !jfound && L.used >= C::CAPI) return 2;  // table full: hand over before step zs
+  if (!slow) {
+    if (moved) {
+      tab_put<C>(mytab, bj * 4 + jway, (ji << 16) | (vz - 1));
+      L.used += !jfound;
+    }
+    Reg* r = &L.regs[vj - 1];
+    const u64 ty = (u64)__double_as_longlong(L.t);
+    u64 cy, cid;
+    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
+                 : "=l"(cy), "=l"(cid) : "r"((u32)__cvta_generic_to_shared(r)) : "memory");
+    if (lex_less(ty, L.id, cy, cid)) {
+      cas128_shared(r, cy, cid, ty, L.id, L.poy, L.poid);
+      L.pr = r;
+      L.pcy = cy;
+      L.pcid = cid;
+      L.pny = ty;
+      L.pnid = L.id;
+    }
+  } else {
+    if (!lane_step_generic<C>(L, zs, L.t, mytab, k)) return 2;
+  }
+  if (!L.fast) dq2 = __ddiv_rn(L2, D2);
+  // advance: pending arrival of step zs + 1 from the spacing computed last call
+  L.b = L.t;
+  L.z = zs;
+  L.jz = jn;
+  const double dqn = L.dqn;
+  L.dqn = dq2;
+  L.t = zs < k ? __dadd_rn(L.b, dqn) : __longlong_as_double(0x7FF0000000000000ll);
   const int rc = (L.z >= k || L.t > L.tau) ? 1 : 0;
   if (rc) lane_settle(L);  // the element is counted as finished after this call
   return rc;
@@ -378,12 +514,14 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 
   u32* tables = reinterpret_cast<u32*>(smem_raw + (size_t)V * k * sizeof(Reg));
   u32* mtab = tables + (size_t)NT * C::SLOTS;
-  double* scan = reinterpret_cast<double*>(mtab + C::MTAB) + warp * 32;
-  int* prov = reinterpret_cast<int*>(reinterpret_cast<double*>(mtab + C::MTAB) + NWARP * 32) + warp * 32;
+  double (*ltab)[4] = reinterpret_cast<double (*)[4]>(mtab + C::MTAB);  // 16-byte aligned: MTAB*4 % 16 == 0
+  double* scan = reinterpret_cast<double*>(ltab + 128) + warp * 32;
+  int* prov = reinterpret_cast<int*>(reinterpret_cast<double*>(ltab + 128) + NWARP * 32) + warp * 32;
   u32* mytab = tables + tid * 4;
   u32* dense = dense_global + ((size_t)blockIdx.x * NWARP + warp) * k;
 
   for (u32 z = tid; z < (u32)C::MTAB; z += NT) mtab[z] = (z >= 1 && z <= k) ? barrett_magic(k - z + 1) : 0u;
+  for (u32 i = tid; i < 128 * 4; i += NT) ltab[i >> 2][i & 3] = gm_logtab[i >> 2][i & 3];
   tab_clear<C>(mytab);
   for (u32 i = lane; i < k; i += 32) dense[i] = 0;  // stamps restart every launch
   if (tid < V) {
@@ -658,7 +796,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 #pragma unroll 1
     for (int u = 0; u < C::U; ++u) {
       if (live) {
-        const int rc = lane_step<C>(L, fresh, mytab, mtab, k);
+        const int rc = lane_step<C>(L, fresh, mytab, mtab, k, ltab);
         fresh = false;
         if (rc == 1) {
           em += L.z < k ? L.z + 1 : L.z;
