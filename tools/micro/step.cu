@@ -4,13 +4,15 @@
 #include <cuda_runtime.h>
 #include "../../paper_2302_05176_b200/csrc/gm_csr.cuh"
 using namespace gmk;
-using C = CsrCfg<256, 8, 2, 4>;
+using C = CsrCfg<256, 16, 2, 2>;
 
-__global__ void __launch_bounds__(256, 4) kstep(unsigned long long* cyc, unsigned long long* steps_out, int iters, u32 k) {
+__global__ void __launch_bounds__(256, 2) kstep(unsigned long long* cyc, unsigned long long* steps_out, int iters, u32 k) {
   extern __shared__ __align__(16) unsigned char sm[];
   Reg* regs = reinterpret_cast<Reg*>(sm);
   u32* tables = reinterpret_cast<u32*>(sm + (size_t)k * 16);
   u32* mtab = tables + 256 * C::SLOTS;
+  double (*ltab)[4] = reinterpret_cast<double (*)[4]>(mtab + C::MTAB);
+  for (u32 i = threadIdx.x; i < 512; i += blockDim.x) ltab[i >> 2][i & 3] = gm_logtab[i >> 2][i & 3];
   for (u32 z = threadIdx.x; z < (u32)C::MTAB; z += blockDim.x) mtab[z] = (z >= 1 && z <= k) ? barrett_magic(k - z + 1) : 0u;
   for (u32 j = threadIdx.x; j < k; j += blockDim.x) { regs[j].y = INF_BITS; regs[j].id = NO_ID; }
   u32* mytab = tables + threadIdx.x * 4;
@@ -30,20 +32,26 @@ __global__ void __launch_bounds__(256, 4) kstep(unsigned long long* cyc, unsigne
   __syncwarp();
   long long t0 = clock64();
   for (int i = 0; i < iters; ++i) {
-    const int rc = lane_step<C>(L, fresh, mytab, mtab, k);
-    fresh = false;
+#ifdef LA
+    u32 em = 0;
+    const int rc = lane_step_la<C, 4>(L, mytab, mtab, k, ltab, em);
+    nsteps += 4;
+#else
+    const int rc = lane_step<C>(L, fresh, mytab, mtab, k, ltab);
     ++nsteps;
+#endif
+    fresh = false;
     if (rc) start();
   }
   long long t1 = clock64();
-  if ((threadIdx.x & 31) == 0) { atomicAdd(cyc, (unsigned long long)(t1 - t0)); atomicAdd(steps_out, (unsigned long long)iters); }
+  if ((threadIdx.x & 31) == 0) { atomicAdd(cyc, (unsigned long long)(t1 - t0)); atomicAdd(steps_out, (unsigned long long)nsteps); }
 }
 
 int main() {
   unsigned long long *cyc, *st;
   cudaMalloc(&cyc, 8); cudaMalloc(&st, 8);
   const u32 k = 1024;
-  const size_t smem = (size_t)k * 16 + 256 * C::SLOTS * 4 + C::MTAB * 4;
+  const size_t smem = (size_t)k * 16 + 256 * C::SLOTS * 4 + C::MTAB * 4 + 4096;
   cudaFuncSetAttribute(kstep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   for (int warps : {1, 2, 4, 8}) {
     for (int rep = 0; rep < 2; ++rep) {
@@ -55,7 +63,7 @@ int main() {
       if (rep) printf("warps/SM %2d: %7.1f cycles per warp-step (%s)\n", warps, (double)c / s, cudaGetErrorString(cudaGetLastError()));
     }
   }
-  for (int ctas : {2, 3, 4}) for (int rep = 0; rep < 2; ++rep) {
+  for (int ctas : {2}) for (int rep = 0; rep < 2; ++rep) {
     cudaMemset(cyc, 0, 8); cudaMemset(st, 0, 8);
     kstep<<<148 * ctas, 256, smem>>>(cyc, st, 2000, k);
     cudaDeviceSynchronize();
