@@ -55,6 +55,7 @@ extern "C" {
 #define GM_FLAG_ASYNC 0x1u       /* enqueue only; see gm_stream_status()           */
 #define GM_FLAG_EXHAUSTIVE 0x2u  /* run every queue to k (sketch_naive semantics)  */
 #define GM_FLAG_ACCUMULATE 0x4u  /* gm_sketch_elements: fold into y_io/s_io        */
+#define GM_FLAG_SPLIT 0x8u       /* gm_sketch_csr: experimental split schedule     */
 
 /* Library version (major*10000 + minor*100 + patch). */
 int gm_version(void);

@@ -55,6 +55,7 @@ from .sketch import (
     check_compatible,
     compute_ri,
     sketch_csr,
+    sketch_csr_host,
     sketch_elements,
     sketch_fast,
     sketch_fast_counted,

@@ -14,6 +14,9 @@
 
 #include "../../include/gmsketch_b200.h"
 #include "gm_csr.cuh"
+#include "gm_split.cuh"
+
+#include <cub/device/device_scan.cuh>
 
 using namespace gmk;
 
@@ -52,6 +55,28 @@ struct Workspace {
   size_t dense_cap = 0;
   u32* resume = nullptr;
   size_t resume_cap = 0;
+  // split CSR path
+  u32* sp_vec = nullptr;                   // element -> vector
+  size_t sp_vec_cap = 0;
+  u32* sp_depth = nullptr;                 // accepted arrivals per element
+  size_t sp_depth_cap = 0;
+  unsigned long long* sp_aoff = nullptr;   // exclusive scan of depth
+  size_t sp_aoff_cap = 0;
+  void* sp_scan_tmp = nullptr;
+  size_t sp_scan_cap = 0;
+  double* sp_t = nullptr;                  // arrival times
+  size_t sp_t_cap = 0;
+  unsigned short* sp_j = nullptr;          // draws j - 1
+  size_t sp_j_cap = 0;
+  u32* sp_e = nullptr;                     // element of each arrival
+  size_t sp_e_cap = 0;
+  Reg* sp_regs = nullptr;                  // registers of the batch
+  size_t sp_regs_cap = 0;
+  u32* sp_dense = nullptr;                 // fy_kernel carry arrays
+  size_t sp_dense_cap = 0;
+  int* sp_redo = nullptr;                  // vectors to re-run
+  size_t sp_redo_cap = 0;
+  unsigned long long* sp_ctr = nullptr;    // [0..2] feeders, [3] n_redo (int), [4] total arrivals
   u32* csr_dense = nullptr;                // CSR warp-walker dense arrays (stamped)
   size_t csr_dense_cap = 0;
   double* vsum = nullptr;                  // per-vector total weight (CSR prep)
@@ -103,9 +128,9 @@ int grow(T** p, size_t* cap, size_t need, cudaStream_t st, bool zero = false) {
   return GM_OK;
 }
 
-int map_device_error(unsigned long long e) {
+int map_device_error(unsigned long long e, unsigned long long vec_base = 0) {
   const int code = (int)(e & 0xFFFFFFFFull);
-  const unsigned long long where = e >> 32;
+  const unsigned long long where = (e >> 32) + (code == GM_ERR_EMPTY_VECTOR || code == 3 ? vec_base : 0);
   switch (code) {
     case GM_ERR_EMPTY_VECTOR:
       return fail(code, "EmptyVectorError: vector %llu has no positive entries", where);
@@ -120,7 +145,7 @@ int map_device_error(unsigned long long e) {
 }
 
 // reads and clears the latched error word; synchronises st
-int check_sync(Workspace* ws, cudaStream_t st) {
+int check_sync(Workspace* ws, cudaStream_t st, unsigned long long vec_base = 0) {
   CK(cudaMemcpyAsync(ws->host, ws->err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   CK(cudaGetLastError());
@@ -128,7 +153,7 @@ int check_sync(Workspace* ws, cudaStream_t st) {
   if (e) {
     CK(cudaMemsetAsync(ws->err, 0, sizeof(unsigned long long), st));
     CK(cudaStreamSynchronize(st));
-    return map_device_error(e);
+    return map_device_error(e, vec_base);
   }
   return GM_OK;
 }
@@ -161,7 +186,7 @@ int csr_cfg_choice() {
 template <class C, class IdT, class WT>
 int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k,
                u64 useed, u64 pseed, double* y, u64* s, int64_t* em, Workspace* ws,
-               cudaStream_t st, int attempt0) {
+               cudaStream_t st, int attempt0, const int* vec_list = nullptr, bool skip_prep = false) {
   auto kern = csr3_kernel<C, IdT, WT>;
   const size_t smem = csr3_smem_bytes<C>(k);
   int per_sm = 0;
@@ -202,14 +227,80 @@ int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n
   rc = grow(&ws->vflag, &ws->vflag_cap, (size_t)n_vec, st);
   if (rc) return rc;
   CK(cudaMemsetAsync(ws->counters, 0, sizeof(int), st));
-  const int64_t prep_blocks = std::min<int64_t>((n_vec + 7) / 8, (int64_t)num_sms() * 16);
-  csr_prep_kernel<WT><<<(unsigned)prep_blocks, 256, 0, st>>>((const WT*)w, offsets, n_vec, ws->vsum, ws->vflag,
-                                                             ws->err);
-  CK(cudaGetLastError());
+  if (!skip_prep) {
+    const int64_t prep_blocks = std::min<int64_t>((n_vec + 7) / 8, (int64_t)num_sms() * 16);
+    csr_prep_kernel<WT><<<(unsigned)prep_blocks, 256, 0, st>>>((const WT*)w, offsets, n_vec, ws->vsum, ws->vflag,
+                                                               ws->err);
+    CK(cudaGetLastError());
+  }
   kern<<<(unsigned)grid, C::NT, smem, st>>>((const IdT*)ids, (const WT*)w, offsets, n_vec, k, useed, pseed,
                                             ws->vsum, ws->vflag, y, s, em, ws->counters, ws->csr_dense, ws->err,
-                                            attempt0);
+                                            attempt0, vec_list);
   CK(cudaGetLastError());
+  return GM_OK;
+}
+
+// Split CSR path (gm_split.cuh): depth pass, scan, arrival pass, Fisher-Yates
+// pass, finalize; vectors whose pass left a register unset are re-run with a
+// larger tau through the fused kernel.  Two host syncs (element count and
+// re-run count).
+template <class IdT, class WT>
+int launch_split(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k, u64 useed,
+                 u64 pseed, double* y, u64* s, int64_t* em, Workspace* ws, cudaStream_t st, int attempt0) {
+  int64_t n = 0;
+  CK(cudaMemcpyAsync(&n, offsets + n_vec, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int rc;
+  if ((rc = grow(&ws->sp_vec, &ws->sp_vec_cap, (size_t)n + 1, st))) return rc;
+  if ((rc = grow(&ws->sp_depth, &ws->sp_depth_cap, (size_t)n + 1, st))) return rc;
+  if ((rc = grow(&ws->sp_aoff, &ws->sp_aoff_cap, (size_t)n + 1, st))) return rc;
+  if ((rc = grow(&ws->sp_regs, &ws->sp_regs_cap, (size_t)n_vec * k, st))) return rc;
+  if ((rc = grow(&ws->vsum, &ws->vsum_cap, (size_t)n_vec, st))) return rc;
+  if ((rc = grow(&ws->vflag, &ws->vflag_cap, (size_t)n_vec, st))) return rc;
+  if ((rc = grow(&ws->sp_redo, &ws->sp_redo_cap, (size_t)n_vec, st))) return rc;
+  if (!ws->sp_ctr) CK(cudaMalloc(&ws->sp_ctr, 8 * sizeof(unsigned long long)));
+  const int sms = num_sms();
+  const int64_t grid_v = std::min<int64_t>((n_vec + 7) / 8, (int64_t)sms * 16);
+  csr_prep_kernel<WT><<<(unsigned)grid_v, 256, 0, st>>>((const WT*)w, offsets, n_vec, ws->vsum, ws->vflag, ws->err);
+  vec_of_kernel<<<(unsigned)grid_v, 256, 0, st>>>(offsets, n_vec, ws->sp_vec);
+  regs_init_kernel<<<sms * 8, 256, 0, st>>>(ws->sp_regs, n_vec * (int64_t)k);
+  CK(cudaMemsetAsync(ws->sp_ctr, 0, 8 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(ws->sp_depth + n, 0, sizeof(u32), st));
+  const unsigned grid_a = (unsigned)(sms * 8);
+  arrivals_kernel<IdT, WT, false><<<grid_a, SPLIT_NT, 0, st>>>(
+      (const IdT*)ids, (const WT*)w, n, ws->sp_vec, ws->vsum, ws->vflag, k, useed, pseed, attempt0, ws->sp_depth,
+      nullptr, 0, nullptr, nullptr, nullptr, ws->sp_ctr + 0);
+  CK(cudaGetLastError());
+  size_t tmp = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ws->sp_depth, ws->sp_aoff, (int64_t)n + 1, st));
+  if ((rc = grow((unsigned char**)&ws->sp_scan_tmp, &ws->sp_scan_cap, tmp, st))) return rc;
+  CK(cub::DeviceScan::ExclusiveSum(ws->sp_scan_tmp, tmp, ws->sp_depth, ws->sp_aoff, (int64_t)n + 1, st));
+  unsigned long long total = 0;
+  CK(cudaMemcpyAsync(&total, ws->sp_aoff + n, sizeof(total), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if ((rc = grow(&ws->sp_t, &ws->sp_t_cap, (size_t)total + 1, st))) return rc;
+  if ((rc = grow(&ws->sp_j, &ws->sp_j_cap, (size_t)total + 1, st))) return rc;
+  if ((rc = grow(&ws->sp_e, &ws->sp_e_cap, (size_t)total + 1, st))) return rc;
+  arrivals_kernel<IdT, WT, true><<<grid_a, SPLIT_NT, 0, st>>>(
+      (const IdT*)ids, (const WT*)w, n, ws->sp_vec, ws->vsum, ws->vflag, k, useed, pseed, attempt0, ws->sp_depth,
+      ws->sp_aoff, (unsigned long long)ws->sp_t_cap, ws->sp_t, ws->sp_j, ws->sp_e, ws->sp_ctr + 1);
+  CK(cudaGetLastError());
+  const unsigned grid_b = (unsigned)(sms * 8);
+  if ((rc = grow(&ws->sp_dense, &ws->sp_dense_cap, (size_t)grid_b * (SPLIT_NT / 32) * k, st))) return rc;
+  fy_kernel<IdT><<<grid_b, SPLIT_NT, 0, st>>>((const IdT*)ids, n, ws->sp_vec, ws->sp_aoff, ws->sp_t, ws->sp_j,
+                                              ws->sp_e, k, ws->sp_regs, ws->sp_dense, ws->sp_ctr + 2);
+  CK(cudaGetLastError());
+  finalize_kernel<<<(unsigned)grid_v, 256, 0, st>>>(ws->sp_regs, n_vec, k, y, s, ws->sp_redo, (int*)(ws->sp_ctr + 3));
+  if (em) split_emitted_kernel<<<(unsigned)grid_v, 256, 0, st>>>(offsets, n_vec, ws->sp_depth, k, em);
+  CK(cudaGetLastError());
+  int n_redo = 0;
+  CK(cudaMemcpyAsync(&n_redo, ws->sp_ctr + 3, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (n_redo > 0) {  // a larger tau for those vectors, fused kernel (weights already validated)
+    rc = launch_csr<CsrDefault, IdT, WT>(ids, w, offsets, n_redo, k, useed, pseed, y, s, em, ws, st,
+                                          attempt0 + 1, ws->sp_redo, true);
+    if (rc) return rc;
+  }
   return GM_OK;
 }
 
@@ -380,7 +471,16 @@ int gm_sketch_csr(const void* ids, int id_bits, const void* w, int w_bits, const
   const u32 kk = (u32)k;
   // exhaustive = a single pass with tau = +inf (pass_tau's last attempt)
   const int a0 = (flags & GM_FLAG_EXHAUSTIVE) ? 3 : 0;
-  if (id_bits == 32 && w_bits == 32)
+  if ((flags & GM_FLAG_SPLIT) && !(flags & GM_FLAG_EXHAUSTIVE)) {
+    if (id_bits == 32 && w_bits == 32)
+      rc = launch_split<u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
+    else if (id_bits == 32)
+      rc = launch_split<u32, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
+    else if (w_bits == 32)
+      rc = launch_split<u64, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
+    else
+      rc = launch_split<u64, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
+  } else if (id_bits == 32 && w_bits == 32)
     switch (csr_cfg_choice()) {
       case 1: rc = launch_csr<CsrAlt1, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0); break;
       case 2: rc = launch_csr<CsrAlt2, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0); break;

@@ -418,10 +418,11 @@ __device__ __forceinline__ void slot_open_pass(SlotInfo& sl, u32 k, int attempt,
 
 // warp-uniform: take the next vector of the batch into slot s (or mark it
 // empty when the batch is exhausted)
+
 template <class C>
 __device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const int64_t* offsets,
                           int64_t n_vec, const double* Wsum, const int* vflags, int* vec_counter,
-                          unsigned long long* err, int attempt0, int lane) {
+                          unsigned long long* err, int attempt0, int lane, const int* vec_list) {
   const unsigned FULL = 0xFFFFFFFFu;
   SlotInfo& sl = S.slot[s];
   for (;;) {
@@ -437,6 +438,7 @@ __device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const
       __syncwarp();
       return;
     }
+    if (vec_list) v = vec_list[v];  // a subset of the batch (re-runs)
     const int64_t lo = offsets[v], n = offsets[v + 1] - lo;
     if (n <= 0) continue;  // EmptyVectorError latched by the prep kernel
     if (n > C::NMAX) {
@@ -504,7 +506,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
                 const double* __restrict__ Wsum, const int* __restrict__ vflags,
                 double* __restrict__ y_out, u64* __restrict__ s_out,
                 int64_t* __restrict__ emitted_out, int* __restrict__ vec_counter,
-                u32* __restrict__ dense_global, unsigned long long* __restrict__ err, int attempt0) {
+                u32* __restrict__ dense_global, unsigned long long* __restrict__ err, int attempt0,
+                const int* __restrict__ vec_list) {
   constexpr int NT = C::NT, NWARP = C::NWARP, V = C::V;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ CsrShared S;
@@ -532,7 +535,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   }
   if (tid == 0) S.seq = 0;
   __syncthreads();
-  if (warp < V) slot_load<C>(S, warp, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane);
+  if (warp < V) slot_load<C>(S, warp, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list);
   __syncthreads();
 
   Lane L;
@@ -607,7 +610,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       }
       if (emitted_out && lane == 0) emitted_out[v] = (int64_t)sl.emitted;
       __syncwarp();
-      slot_load<C>(S, s, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane);
+      slot_load<C>(S, s, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list);
     }
 
 #ifdef GM_STATS
@@ -699,8 +702,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         const u32 got = min(room, n - i0);
         const u32 t = (u32)lane - qnext;  // this lane's offset in the new run
         if (t < got) {
-          const u64 id = (u64)__ldg(&ids[lo + i0 + t]);
-          const double w = (double)__ldg(&wts[lo + i0 + t]);
+          // L2-only loads: each element is read once
+          const u64 id = (u64)__ldcg(&ids[lo + i0 + t]);
+          const double w = (double)__ldcg(&wts[lo + i0 + t]);
           if (qcur) {
             qa_slot = s;
             qa_id = id;

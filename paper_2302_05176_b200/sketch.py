@@ -194,13 +194,14 @@ def _check_k(k: int) -> None:
 
 
 def sketch_csr(ids, weights, offsets, k: int, scheme: SeedScheme, *, exhaustive: bool = False,
-               counted: bool = False, asynchronous: bool = False) -> SketchBatch:
+               counted: bool = False, asynchronous: bool = False, split: bool = False) -> SketchBatch:
     """Sketch every CSR vector ids[offsets[v]:offsets[v+1]] on the device.
 
     ids: uint32/uint64 (or int32/int64 viewed as unsigned) tensor or array;
     weights: float32/float64; offsets: int64 [n_vec + 1].  Ids must be
     distinct within a vector (WeightedVector keys).  Device tensors are used
-    in place; host arrays are copied in."""
+    in place; host arrays are copied in.  ``split=True`` selects the
+    experimental split schedule; results are identical."""
     _check_k(k)
     dev = _device.require_cuda()
     ids_t = ids if isinstance(ids, torch.Tensor) else torch.from_numpy(_as_id_np(ids))
@@ -214,12 +215,59 @@ def sketch_csr(ids, weights, offsets, k: int, scheme: SeedScheme, *, exhaustive:
     y = torch.empty((n_vec, k), dtype=torch.float64, device=dev)
     s = torch.empty((n_vec, k), dtype=torch.int64, device=dev)
     em = torch.empty(n_vec, dtype=torch.int64, device=dev) if counted else None
-    flags = (_lib.GM_FLAG_EXHAUSTIVE if exhaustive else 0) | (_lib.GM_FLAG_ASYNC if asynchronous else 0)
+    flags = ((_lib.GM_FLAG_EXHAUSTIVE if exhaustive else 0) | (_lib.GM_FLAG_ASYNC if asynchronous else 0)
+             | (_lib.GM_FLAG_SPLIT if split else 0))
     _device.call("gm_sketch_csr", ids_t.data_ptr(), _device.id_bits_of(ids_t), w_t.data_ptr(),
                  _device.w_bits_of(w_t), off_t.data_ptr(), n_vec, k, scheme.global_seed,
                  scheme.stream_salt, flags, y.data_ptr(), s.data_ptr(), _device.ptr(em),
                  _device.stream_ptr())
     return SketchBatch(k, y, s, scheme.fingerprint, em)
+
+
+def sketch_csr_host(ids, weights, offsets, k: int, scheme: SeedScheme, *, out=None,
+                    counted: bool = False, exhaustive: bool = False):
+    """Host-buffer batch: ``sketch_csr`` for CPU-resident CSR arrays, through
+    gm_sketch_csr_host (input copies pipelined with the sketch; results
+    stored straight into page-locked outputs).  ``out=(y, s)`` supplies
+    output arrays or CPU tensors (float64 / uint64-or-int64, shape
+    [n_vec, k]); pin them for the zero-copy store.  Returns (y, s, emitted
+    or None) as given/allocated (numpy when allocated here)."""
+    _check_k(k)
+    _device.require_cuda()
+
+    def host(a, dt):
+        if isinstance(a, torch.Tensor):
+            assert a.device.type == "cpu" and a.is_contiguous(), "host tensors must be contiguous CPU tensors"
+            return a, a.data_ptr()
+        a = np.ascontiguousarray(a, dtype=dt) if dt is not None else np.ascontiguousarray(a)
+        return a, a.ctypes.data
+
+    if isinstance(ids, torch.Tensor):
+        id_bits = _device.id_bits_of(ids)
+        ids_h, ip = host(ids, None)
+    else:
+        a, id_bits = _device.id_array(ids)
+        ids_h, ip = host(a, None)
+    if isinstance(weights, torch.Tensor):
+        w_bits = _device.w_bits_of(weights)
+        w_h, wp = host(weights, None)
+    else:
+        a, w_bits = _device.weight_array(weights)
+        w_h, wp = host(a, None)
+    off_h, op = host(offsets, None) if isinstance(offsets, torch.Tensor) else host(offsets, np.int64)
+    n_vec = int(off_h.shape[0]) - 1
+    if out is None:
+        y, s = np.empty((n_vec, k), np.float64), np.empty((n_vec, k), np.uint64)
+    else:
+        y, s = out
+    _, yp = host(y, None)
+    _, sp = host(s, None)
+    em = np.zeros(max(n_vec, 1), np.int64) if counted else None
+    flags = _lib.GM_FLAG_EXHAUSTIVE if exhaustive else 0
+    _device.call("gm_sketch_csr_host", ip, id_bits, wp, w_bits, op, n_vec, k, scheme.global_seed,
+                 scheme.stream_salt, flags, yp, sp, em.ctypes.data if em is not None else None,
+                 _device.stream_ptr())
+    return y, s, (em[:n_vec] if em is not None else None)
 
 
 def _as_id_np(ids) -> np.ndarray:

@@ -247,6 +247,47 @@ def test_csr_vs_elements_kernels_agree():
         assert_regs(y2.cpu().numpy(), s2.cpu().numpy().view(np.uint64), y[v], s[v], tol=0.0)
 
 
+def test_split_schedule_equals_fused():
+    """The experimental split schedule (GM_FLAG_SPLIT) returns the fused
+    kernel's registers bit for bit, including vectors that need a second pass."""
+    for ids, w, off, k, seed in (workloads.config2(), workloads.config3(n_vectors=2000)):
+        sc = gm.SeedScheme(seed)
+        a = gm.sketch_csr(ids, w, off, k, sc)
+        b = gm.sketch_csr(ids, w, off, k, sc, split=True)
+        assert torch.equal(a.s, b.s) and torch.equal(a.y, b.y)
+    rng = np.random.default_rng(4)
+    for n, k in [(3, 512), (50, 8192), (400, 65536)]:
+        ids = rng.choice(10**9, n, replace=False).astype(np.uint64) + 1
+        w = np.exp(rng.normal(0, 6, n))
+        a = gm.sketch_csr(ids, w, np.array([0, n]), k, gm.SeedScheme(9))
+        b = gm.sketch_csr(ids, w, np.array([0, n]), k, gm.SeedScheme(9), split=True)
+        assert torch.equal(a.s, b.s) and torch.equal(a.y, b.y)
+
+
+def test_host_api_matches_device_api():
+    """gm_sketch_csr_host (pinned zero-copy or pageable outputs) returns the
+    device path's registers bit for bit and reports data errors with the
+    batch's vector indices."""
+    ids, w, off, k, seed = workloads.config2()
+    sc = gm.SeedScheme(seed)
+    d = gm.sketch_csr(ids, w, off, k, sc, counted=True)
+    y, s, em = gm.sketch_csr_host(ids, w, off, k, sc, counted=True)
+    assert np.array_equal(s, d.s.cpu().numpy().view(np.uint64)) and np.array_equal(y, d.y.cpu().numpy())
+    assert em.tolist() == d.emitted.cpu().tolist()
+    n_vec = len(off) - 1
+    yp = torch.empty((n_vec, k), dtype=torch.float64).pin_memory()
+    sp = torch.empty((n_vec, k), dtype=torch.int64).pin_memory()
+    gm.sketch_csr_host(torch.from_numpy(ids).pin_memory(), torch.from_numpy(w).pin_memory(),
+                       torch.from_numpy(off), k, sc, out=(yp, sp))
+    assert torch.equal(sp, d.s.cpu()) and torch.equal(yp, d.y.cpu())
+    bad = off.copy()
+    bad[900] = bad[899]  # vector 899 empty
+    with pytest.raises(gm.EmptyVectorError, match="vector 899"):
+        gm.sketch_csr_host(ids, w, bad, k, sc)
+    y2, s2, _ = gm.sketch_csr_host(ids, w, off, k, sc)  # the error does not stick
+    assert np.array_equal(s2, s)
+
+
 # ---------------------------------------------------------------- edge cases
 def test_single_element_owns_every_register():
     for k in (1, 3, 64, 1024, 4096):
