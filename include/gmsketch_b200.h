@@ -161,6 +161,22 @@ int gm_arith_check(int64_t n, uint64_t seed, unsigned long long *counts,
                    void *stream);
 int gm_log_batch(const double *x, int64_t n, double *out, void *stream);
 
+/* Exact-y finalize (host memory only; no CUDA): y_io[v*k + j] := the
+ * arrival time the reference computes for register j of CSR vector v,
+ * given its winning element s[v*k + j] (from gm_sketch_csr* /
+ * gm_sketch_elements), by walking that element's queue with glibc log and
+ * IEEE double arithmetic in the reference's operation order
+ * (randgen.py:158-207).  The device's y can differ from the reference's by
+ * an ulp (its log is CUDA's); after this call y is bit-identical.  Every
+ * s must name an element of its vector (else GM_ERR_MISMATCHED).  For a
+ * stream, pass n_vec = 1 and offsets {0, n}.  n_threads <= 0: all host
+ * threads.  Replaces the float equality of GumbelMaxSketch
+ * (sketch.py:118-136) for sketches built on the device. */
+int gm_exact_y(const void *ids, int id_bits, const void *w, int w_bits,
+               const int64_t *offsets, int64_t n_vec, int32_t k,
+               uint64_t global_seed, uint64_t stream_salt, const uint64_t *s,
+               double *y_io, int32_t n_threads);
+
 /* Work counters of a library built with -DGM_STATS (tools/stats.py): copies
  * and clears 16 u64 host words; GM_ERR_INVALID_PARAMETER in normal builds. */
 int gm_stats_read(unsigned long long *out16);

@@ -56,6 +56,7 @@ from .sketch import (
     compute_ri,
     sketch_csr,
     sketch_csr_host,
+    exact_y_host,
     sketch_elements,
     sketch_fast,
     sketch_fast_counted,

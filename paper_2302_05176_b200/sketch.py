@@ -12,7 +12,11 @@ Generators run on the device:
   sketch_csr / sketch_many            -> batched K1 over CSR arrays (new; the
                                          reference callers loop per vector)
 Registers equal the reference's: s bit-exact; y within the documented
-tolerance (the device log is CUDA's, not glibc's).
+tolerance (the device log is CUDA's, not glibc's), and
+bit-identical after the exact-y finalize (exact_y_host, gm_exact_y), which
+the reference-typed entry points (sketch_fast/naive, sketch_stream,
+sketch_pairs) always apply so GumbelMaxSketch equality holds against the
+reference's own sketches.
 The *_counted work counters count arrivals the device computed, which is
 schedule-dependent and differs from the reference's FastSearch count.
 """
@@ -194,14 +198,17 @@ def _check_k(k: int) -> None:
 
 
 def sketch_csr(ids, weights, offsets, k: int, scheme: SeedScheme, *, exhaustive: bool = False,
-               counted: bool = False, asynchronous: bool = False, split: bool = False) -> SketchBatch:
+               counted: bool = False, asynchronous: bool = False, split: bool = False,
+               exact_y: bool = False) -> SketchBatch:
     """Sketch every CSR vector ids[offsets[v]:offsets[v+1]] on the device.
 
     ids: uint32/uint64 (or int32/int64 viewed as unsigned) tensor or array;
     weights: float32/float64; offsets: int64 [n_vec + 1].  Ids must be
     distinct within a vector (WeightedVector keys).  Device tensors are used
     in place; host arrays are copied in.  ``split=True`` selects the
-    experimental split schedule; results are identical."""
+    experimental split schedule; results are identical.
+    ``exact_y=True`` re-derives y on the host with the reference's
+    arithmetic (exact_y_host): bit-identical y, at host cost."""
     _check_k(k)
     dev = _device.require_cuda()
     ids_t = ids if isinstance(ids, torch.Tensor) else torch.from_numpy(_as_id_np(ids))
@@ -221,17 +228,22 @@ def sketch_csr(ids, weights, offsets, k: int, scheme: SeedScheme, *, exhaustive:
                  _device.w_bits_of(w_t), off_t.data_ptr(), n_vec, k, scheme.global_seed,
                  scheme.stream_salt, flags, y.data_ptr(), s.data_ptr(), _device.ptr(em),
                  _device.stream_ptr())
+    if exact_y:
+        y_h = y.cpu()
+        exact_y_host(ids_t.cpu(), w_t.cpu(), off_t.cpu(), k, scheme, s.cpu(), y_h)
+        y.copy_(y_h)
     return SketchBatch(k, y, s, scheme.fingerprint, em)
 
 
 def sketch_csr_host(ids, weights, offsets, k: int, scheme: SeedScheme, *, out=None,
-                    counted: bool = False, exhaustive: bool = False):
+                    counted: bool = False, exhaustive: bool = False, exact_y: bool = False):
     """Host-buffer batch: ``sketch_csr`` for CPU-resident CSR arrays, through
     gm_sketch_csr_host (input copies pipelined with the sketch; results
     stored straight into page-locked outputs).  ``out=(y, s)`` supplies
     output arrays or CPU tensors (float64 / uint64-or-int64, shape
     [n_vec, k]); pin them for the zero-copy store.  Returns (y, s, emitted
-    or None) as given/allocated (numpy when allocated here)."""
+    or None) as given/allocated (numpy when allocated here).  ``exact_y``:
+    see sketch_csr."""
     _check_k(k)
     _device.require_cuda()
 
@@ -267,7 +279,35 @@ def sketch_csr_host(ids, weights, offsets, k: int, scheme: SeedScheme, *, out=No
     _device.call("gm_sketch_csr_host", ip, id_bits, wp, w_bits, op, n_vec, k, scheme.global_seed,
                  scheme.stream_salt, flags, yp, sp, em.ctypes.data if em is not None else None,
                  _device.stream_ptr())
+    if exact_y:
+        exact_y_host(ids_h, w_h, off_h, k, scheme, s, y)
     return y, s, (em[:n_vec] if em is not None else None)
+
+
+def exact_y_host(ids, weights, offsets, k: int, scheme: SeedScheme, s, y, threads: int = 0):
+    """Re-derive registers' values with the reference's arithmetic (glibc log,
+    randgen.py:158-207) from their winning elements, in place: y becomes
+    bit-identical to the reference's (gm_exact_y; host arrays, no device
+    work).  s: uint64/int64 [n_vec, k] (or [k]), y: float64 of the same
+    shape; CPU tensors or numpy arrays."""
+    def np_of(a):
+        return a.numpy() if isinstance(a, torch.Tensor) else a
+
+    a_ids, id_bits = _device.id_array(np_of(ids).view(np.uint32) if np_of(ids).dtype == np.int32 else np_of(ids))
+    a_w, w_bits = _device.weight_array(np_of(weights))
+    off = np.ascontiguousarray(np.asarray(np_of(offsets), dtype=np.int64))
+    s_np = np.ascontiguousarray(np_of(s)).view(np.uint64)
+    y_np = np_of(y)
+    assert y_np.dtype == np.float64 and y_np.flags.c_contiguous, "y must be a contiguous float64 array"
+    assert s_np.size == y_np.size == (off.size - 1) * k, "s, y must hold k registers per vector"
+    rc = _lib.load().gm_exact_y(a_ids.ctypes.data, id_bits, a_w.ctypes.data, w_bits, off.ctypes.data,
+                                off.size - 1, k, scheme.global_seed, scheme.stream_salt, s_np.ctypes.data,
+                                y_np.ctypes.data, threads)
+    if rc == _lib.GM_ERR_MISMATCHED:
+        raise MismatchedSketchError("a register names an element that is not in its vector")
+    if rc:
+        raise InvalidParameterError(f"gm_exact_y failed with code {rc}")
+    return y
 
 
 def _as_id_np(ids) -> np.ndarray:
@@ -310,13 +350,15 @@ def _sketch_vector(v: WeightedVector, params: GenerationParams, exhaustive: bool
         raise EmptyVectorError("cannot sketch a vector with no positive entries")
     ids, w = v.arrays()
     k = params.k
+    off = np.array([0, ids.size], dtype=np.int64)
     if v.n_plus > LARGE_VECTOR:
         y, s, em = sketch_elements(ids, w, k, params.scheme, exhaustive=exhaustive)
-        return _to_sketch(k, y.cpu().numpy(), s.cpu().numpy(), params.scheme.fingerprint), em
+        y, s = y.cpu().numpy(), s.cpu().numpy()
+        exact_y_host(ids, w, off, k, params.scheme, s, y)
+        return _to_sketch(k, y, s, params.scheme.fingerprint), em
     _device.require_cuda()
     bits = 32 if (ids.size and int(ids.max()) < (1 << 32)) else 64
     ids_h = ids.astype(np.uint32) if bits == 32 else ids
-    off = np.array([0, ids.size], dtype=np.int64)
     y = np.empty(k, np.float64)
     s = np.empty(k, np.uint64)
     em = np.zeros(1, np.int64)
@@ -324,6 +366,7 @@ def _sketch_vector(v: WeightedVector, params: GenerationParams, exhaustive: bool
     _device.call("gm_sketch_csr_host", ids_h.ctypes.data, bits, w.ctypes.data, 64, off.ctypes.data, 1,
                  k, params.scheme.global_seed, params.scheme.stream_salt, flags, y.ctypes.data,
                  s.ctypes.data, em.ctypes.data, _device.stream_ptr())
+    exact_y_host(ids_h, w, off, k, params.scheme, s, y)
     return _to_sketch(k, y, s, params.scheme.fingerprint), int(em[0])
 
 
@@ -347,8 +390,10 @@ def sketch_fast_counted(v: WeightedVector, params: GenerationParams):
     return _sketch_vector(v, params, exhaustive=False)
 
 
-def sketch_many(vectors: Sequence[WeightedVector], params: GenerationParams) -> list[GumbelMaxSketch]:
-    """Sketch a list of vectors in one batched launch."""
+def sketch_many(vectors: Sequence[WeightedVector], params: GenerationParams,
+                exact_y: bool = True) -> list[GumbelMaxSketch]:
+    """Sketch a list of vectors in one batched launch (y re-derived with the
+    reference's arithmetic unless ``exact_y=False``)."""
     if not vectors:
         return []
     for v in vectors:
@@ -358,7 +403,7 @@ def sketch_many(vectors: Sequence[WeightedVector], params: GenerationParams) -> 
     w = np.concatenate([v.arrays()[1] for v in vectors])
     off = np.zeros(len(vectors) + 1, dtype=np.int64)
     off[1:] = np.cumsum([v.n_plus for v in vectors])
-    return sketch_csr(ids, w, off, params.k, params.scheme).to_sketches()
+    return sketch_csr(ids, w, off, params.k, params.scheme, exact_y=exact_y).to_sketches()
 
 
 def check_compatible(a: GumbelMaxSketch, b: GumbelMaxSketch) -> None:

@@ -22,7 +22,7 @@ import torch
 from . import _device
 from .errors import IncompleteSketchError, InconsistentWeightError, InvalidParameterError, InvalidWeightError
 from .randgen import MIN_WEIGHT, SeedScheme
-from .sketch import GumbelMaxSketch, sketch_elements
+from .sketch import GumbelMaxSketch, exact_y_host, sketch_elements
 
 StreamItem = tuple[int, float]
 _MASK64 = (1 << 64) - 1
@@ -106,6 +106,12 @@ def stream_finalize(state: StreamSketchState) -> GumbelMaxSketch:
     if state._unset > 0:
         raise IncompleteSketchError([j for j in range(state.k) if math.isinf(y[j])])
     s = state._s.cpu().numpy().view(np.uint64)
+    # y with the reference's arithmetic: the winners' weights are in the
+    # id -> weight dict the stream checks keep
+    win = np.unique(s)
+    wmap = {e & _MASK64: wt for e, wt in state.weights.items()}
+    exact_y_host(win, np.array([wmap[int(e)] for e in win], np.float64), np.array([0, win.size], np.int64),
+                 state.k, state.scheme, s, y)
     alias = state._alias
     s_out = tuple(alias.get(int(x), int(x)) for x in s)
     return GumbelMaxSketch(state.k, s_out, tuple(y.tolist()), state.scheme.fingerprint)
@@ -120,13 +126,14 @@ def sketch_stream(items: Iterable[StreamItem], k: int, scheme: SeedScheme,
     return stream_finalize(state)
 
 
-def sketch_pairs(ids, weights, k: int, scheme: SeedScheme, check: bool = True):
+def sketch_pairs(ids, weights, k: int, scheme: SeedScheme, check: bool = True, exact_y: bool = True):
     """Bulk stream of (id, weight) arrays in one device pass.
 
     With ``check`` the reference's stream checks run vectorised on the host:
     InvalidWeightError for a bad weight and InconsistentWeightError for an id
     that reappears with another weight (raised for the first offending item,
-    like stream_update).  Returns a GumbelMaxSketch."""
+    like stream_update).  ``exact_y`` (default) re-derives y with the
+    reference's arithmetic (sketch.exact_y_host).  Returns a GumbelMaxSketch."""
     a_ids, _ = _device.id_array(ids)
     a_w, _ = _device.weight_array(weights)
     if check and a_ids.size:
@@ -146,8 +153,11 @@ def sketch_pairs(ids, weights, k: int, scheme: SeedScheme, check: bool = True):
         if first_conf is not None:
             raise InconsistentWeightError(f"item {first_conf}: element {int(a_ids[first_conf])} reappeared with another weight")
     y, s, _ = sketch_elements(a_ids, a_w, k, scheme)
-    return GumbelMaxSketch(k, tuple(int(x) for x in s.cpu().numpy().view(np.uint64)),
-                           tuple(y.cpu().numpy().tolist()), scheme.fingerprint)
+    y, s = y.cpu().numpy(), s.cpu().numpy().view(np.uint64)
+    if exact_y:  # only the winners' (id, weight) pairs are scanned by the host walk
+        keep = np.isin(a_ids, np.unique(s))
+        exact_y_host(a_ids[keep], a_w[keep], np.array([0, int(keep.sum())], np.int64), k, scheme, s, y)
+    return GumbelMaxSketch(k, tuple(int(x) for x in s), tuple(y.tolist()), scheme.fingerprint)
 
 
 def parse_stream_items(lines: Iterable[str] | TextIO) -> Iterable[StreamItem]:

@@ -95,8 +95,9 @@ def test_sketch_fast_golden_cases():
         v = gm.WeightedVector({int(e): float(x) for e, x in zip(ids, w)})
         sk = gm.sketch_fast(v, gm.GenerationParams(k=case["k"], scheme=gm.SeedScheme(case["seed"])))
         wy, ws = sketch_arrays(case["fast"])
-        assert_regs(sk.y, np.array(sk.s, np.uint64), wy, ws)
-        assert sk.fingerprint == case["fast"]["fingerprint"]
+        assert_regs(sk.y, np.array(sk.s, np.uint64), wy, ws, tol=0.0)  # exact-y finalize: bit-identical
+        assert sk == gm.GumbelMaxSketch(case["k"], tuple(int(x) for x in ws), tuple(wy.tolist()),
+                                        case["fast"]["fingerprint"])
 
 
 def test_sketch_naive_golden_cases():
@@ -106,7 +107,7 @@ def test_sketch_naive_golden_cases():
         v = gm.WeightedVector({int(e): float(x) for e, x in zip(ids, w)})
         sk, em = gm.sketch_naive_counted(v, gm.GenerationParams(k=case["k"], scheme=gm.SeedScheme(case["seed"])))
         wy, ws = sketch_arrays(case["fast"])
-        assert_regs(sk.y, np.array(sk.s, np.uint64), wy, ws)
+        assert_regs(sk.y, np.array(sk.s, np.uint64), wy, ws, tol=0.0)
         assert em == case["n"] * case["k"]
 
 
@@ -131,7 +132,7 @@ def test_stream_golden_cases():
         items = list(zip(case["ids"], hexs(case["w"]).tolist()))
         sk = gm.sketch_stream(items, case["k"], gm.SeedScheme(case["seed"]))
         wy, ws = sketch_arrays(case["sketch"])
-        assert_regs(sk.y, np.array([int(x) & U64 for x in sk.s], np.uint64), wy, ws)
+        assert_regs(sk.y, np.array([int(x) & U64 for x in sk.s], np.uint64), wy, ws, tol=0.0)
         assert tuple(sk.s) == tuple(case["sketch"]["s"])  # original (possibly huge) ids come back
 
 
@@ -154,7 +155,7 @@ def test_bench_golden():
     assert sim.matches == 9 and sim.value == 0.5625
     assert gm.estimate_cardinality(sks[2]).value == pytest.approx(1.76291929033662, rel=1e-12)
     for sk, want in zip(sks, g["sketches"]):
-        assert_regs(sk.y, np.array(sk.s, np.uint64), *sketch_arrays(want))
+        assert_regs(sk.y, np.array(sk.s, np.uint64), *sketch_arrays(want), tol=0.0)
 
 
 def test_config1_golden():
@@ -166,6 +167,35 @@ def test_config1_golden():
     # the grid-wide kernel agrees too
     y2, s2, _ = gm.sketch_elements(g["ids"].astype(np.uint32), g["w"], int(g["k"]), gm.SeedScheme(int(g["seed"])))
     assert_regs(y2.cpu().numpy(), s2.cpu().numpy().view(np.uint64), g["y"], g["s"])
+
+
+def test_exact_y_batches_bit_exact():
+    """sketch_csr / sketch_csr_host with exact_y: y bit-identical to the
+    reference's arithmetic (oracle, glibc log) on all of config 2."""
+    ids, w, off, k, seed = workloads.config2()
+    sc = gm.SeedScheme(seed)
+    b = gm.sketch_csr(ids, w, off, k, sc, exact_y=True)
+    y, s = batch_np(b)
+    rc, yo, so, _ = O.sketch_csr(ids.astype(np.uint64), w.astype(np.float64), off, k, seed, mode=0, threads=8)
+    assert rc == 0
+    assert np.array_equal(s, so) and y.tobytes() == yo.tobytes()
+    yh, sh, _ = gm.sketch_csr_host(ids, w, off, k, sc, exact_y=True)
+    assert np.array_equal(sh, so) and yh.tobytes() == yo.tobytes()
+    # the device y it replaced was already within the documented tolerance
+    yd, _ = batch_np(gm.sketch_csr(ids, w, off, k, sc))
+    assert_regs(yd, s, yo, so)
+
+
+def test_sketch_pairs_and_many_bit_exact():
+    g = load_npz("config2_sample.npz")
+    vecs = [gm.WeightedVector({int(e): float(x) for e, x in zip(g["ids"][a:b], g["w"][a:b])})
+            for a, b in zip(g["offsets"][:-1], g["offsets"][1:])]
+    params = gm.GenerationParams(k=int(g["k"]), scheme=gm.SeedScheme(int(g["seed"])))
+    for i, sk in enumerate(gm.sketch_many(vecs, params)):
+        assert np.array_equal(np.array(sk.s, np.uint64), g["s"][i]) and list(sk.y) == g["y"][i].tolist()
+    a, b = g["offsets"][0], g["offsets"][1]
+    sk = gm.sketch_pairs(g["ids"][a:b], g["w"][a:b], int(g["k"]), gm.SeedScheme(int(g["seed"])))
+    assert list(sk.y) == g["y"][0].tolist()
 
 
 def test_config2_sample_golden():
