@@ -161,6 +161,20 @@ int gm_arith_check(int64_t n, uint64_t seed, unsigned long long *counts,
                    void *stream);
 int gm_log_batch(const double *x, int64_t n, double *out, void *stream);
 
+/* Stream checks for bulk (id, weight) pairs (device arrays; stream.py:58-78
+ * for every item at once): *first_bad = index of the first item whose weight
+ * is not finite, > 0 and >= 1e-300 (InvalidWeightError), *first_conflict =
+ * index of the first item whose id appeared earlier with another weight
+ * (InconsistentWeightError); -1 when there is none.  With uniq_ids/uniq_w
+ * (device arrays of capacity n, same types as the input; both or neither)
+ * the first occurrence of every id is compacted there (any order) and
+ * *n_uniq is its count: the skip_duplicates input of gm_sketch_elements.
+ * Synchronises `stream`. */
+int gm_check_pairs(const void *ids, int id_bits, const void *w, int w_bits,
+                   int64_t n, int64_t *first_bad, int64_t *first_conflict,
+                   void *uniq_ids, void *uniq_w, int64_t *n_uniq,
+                   void *stream);
+
 /* Exact-y finalize (host memory only; no CUDA): y_io[v*k + j] := the
  * arrival time the reference computes for register j of CSR vector v,
  * given its winning element s[v*k + j] (from gm_sketch_csr* /

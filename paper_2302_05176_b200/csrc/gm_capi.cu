@@ -15,6 +15,7 @@
 #include "../../include/gmsketch_b200.h"
 #include "gm_csr.cuh"
 #include "gm_split.cuh"
+#include "gm_pairs.cuh"
 
 #include <cub/device/device_scan.cuh>
 
@@ -85,6 +86,10 @@ struct Workspace {
   size_t vflag_cap = 0;
   void* stage = nullptr;                   // device staging for *_host calls
   size_t stage_cap = 0;
+  u64* pt_keys = nullptr;                  // gm_check_pairs id table
+  size_t pt_keys_cap = 0;
+  unsigned long long* pt_first = nullptr;
+  size_t pt_first_cap = 0;
 };
 
 std::mutex g_mu;
@@ -404,6 +409,51 @@ int gm_stats_read(unsigned long long* out16) {
   (void)out16;
   return fail(GM_ERR_INVALID_PARAMETER, "library built without GM_STATS");
 #endif
+}
+
+int gm_check_pairs(const void* ids, int id_bits, const void* w, int w_bits, int64_t n, int64_t* first_bad,
+                   int64_t* first_conflict, void* uniq_ids, void* uniq_w, int64_t* n_uniq, void* stream) {
+  g_msg[0] = 0;
+  (void)cudaGetLastError();
+  if ((id_bits != 32 && id_bits != 64) || (w_bits != 32 && w_bits != 64) || n < 0)
+    return fail(GM_ERR_INVALID_PARAMETER, "gm_check_pairs: bad id_bits/w_bits/n");
+  if ((uniq_ids == nullptr) != (uniq_w == nullptr))
+    return fail(GM_ERR_INVALID_PARAMETER, "gm_check_pairs: uniq_ids and uniq_w go together");
+  *first_bad = *first_conflict = -1;
+  if (n_uniq) *n_uniq = 0;
+  if (n == 0) return GM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace* ws = nullptr;
+  int rc = get_ws(st, &ws);
+  if (rc) return rc;
+  size_t cap = 1024;
+  while (cap < 2 * (size_t)n) cap <<= 1;
+  if ((rc = grow(&ws->pt_keys, &ws->pt_keys_cap, cap + 1, st))) return rc;
+  if ((rc = grow(&ws->pt_first, &ws->pt_first_cap, cap + 1, st))) return rc;
+  CK(cudaMemsetAsync(ws->pt_keys, 0xFF, (cap + 1) * sizeof(u64), st));
+  CK(cudaMemsetAsync(ws->pt_first, 0xFF, (cap + 1) * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(ws->ull, 0xFF, 2 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(ws->ull + 2, 0, sizeof(unsigned long long), st));
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+  const u64 mask = cap - 1;
+#define GM_PAIRS(I, W)                                                                                        \
+  do {                                                                                                        \
+    pairs_insert_kernel<I><<<grid, 256, 0, st>>>((const I*)ids, n, ws->pt_keys, ws->pt_first, mask);          \
+    pairs_check_kernel<I, W><<<grid, 256, 0, st>>>((const I*)ids, (const W*)w, n, ws->pt_keys, ws->pt_first, \
+                                                   mask, ws->ull, (I*)uniq_ids, (W*)uniq_w);                  \
+  } while (0)
+  if (id_bits == 32 && w_bits == 32) GM_PAIRS(u32, float);
+  else if (id_bits == 32) GM_PAIRS(u32, double);
+  else if (w_bits == 32) GM_PAIRS(u64, float);
+  else GM_PAIRS(u64, double);
+#undef GM_PAIRS
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(ws->host, ws->ull, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *first_bad = ws->host[0] == ~0ull ? -1 : (int64_t)ws->host[0];
+  *first_conflict = ws->host[1] == ~0ull ? -1 : (int64_t)ws->host[1];
+  if (n_uniq) *n_uniq = (int64_t)ws->host[2];
+  return GM_OK;
 }
 
 int gm_stream_status(void* stream) {

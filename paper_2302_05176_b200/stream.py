@@ -126,33 +126,39 @@ def sketch_stream(items: Iterable[StreamItem], k: int, scheme: SeedScheme,
     return stream_finalize(state)
 
 
-def sketch_pairs(ids, weights, k: int, scheme: SeedScheme, check: bool = True, exact_y: bool = True):
-    """Bulk stream of (id, weight) arrays in one device pass.
+def sketch_pairs(ids, weights, k: int, scheme: SeedScheme, check: bool = True, exact_y: bool = True,
+                 skip_duplicates: bool = True):
+    """Bulk stream of (id, weight) arrays, checked and sketched on the device.
 
-    With ``check`` the reference's stream checks run vectorised on the host:
-    InvalidWeightError for a bad weight and InconsistentWeightError for an id
-    that reappears with another weight (raised for the first offending item,
-    like stream_update).  ``exact_y`` (default) re-derives y with the
-    reference's arithmetic (sketch.exact_y_host).  Returns a GumbelMaxSketch."""
-    a_ids, _ = _device.id_array(ids)
-    a_w, _ = _device.weight_array(weights)
-    if check and a_ids.size:
-        wd = a_w.astype(np.float64)
-        bad = ~(np.isfinite(wd) & (wd > 0.0) & (wd >= MIN_WEIGHT))
-        first_bad = int(np.argmax(bad)) if bad.any() else None
-        order = np.argsort(a_ids, kind="stable")
-        sid = a_ids[order]
-        sw = a_w[order]
-        same = np.concatenate([[False], sid[1:] == sid[:-1]])
-        grp = np.cumsum(~same) - 1
-        first_w = sw[~same][grp]
-        conflict = order[same & (sw != first_w)]
-        first_conf = int(conflict.min()) if conflict.size else None
-        if first_bad is not None and (first_conf is None or first_bad <= first_conf):
+    With ``check`` the reference's stream rules run on the device for every
+    item at once (gm_check_pairs): InvalidWeightError for a bad weight and
+    InconsistentWeightError for an id that reappears with another weight,
+    raised for the first offending item like stream_update.  With
+    ``skip_duplicates`` only first occurrences are sketched (duplicates are
+    register no-ops; stream.py:74-78).  ``exact_y`` (default) re-derives y
+    with the reference's arithmetic (sketch.exact_y_host).  Returns a
+    GumbelMaxSketch."""
+    a_ids, id_bits = _device.id_array(ids)
+    a_w, w_bits = _device.weight_array(weights)
+    dev = _device.require_cuda()
+    ids_t = torch.from_numpy(a_ids.view(np.int32 if id_bits == 32 else np.int64)).to(dev)
+    w_t = torch.from_numpy(a_w).to(dev)
+    if a_ids.size and (check or skip_duplicates):
+        ui = torch.empty_like(ids_t) if skip_duplicates else None
+        uw = torch.empty_like(w_t) if skip_duplicates else None
+        out = np.zeros(3, np.int64)
+        _device.call("gm_check_pairs", ids_t.data_ptr(), id_bits, w_t.data_ptr(), w_bits, a_ids.size,
+                     out[0:].ctypes.data, out[1:].ctypes.data, _device.ptr(ui), _device.ptr(uw),
+                     out[2:].ctypes.data, _device.stream_ptr())
+        first_bad, first_conf, n_uniq = (int(x) for x in out)
+        if check and first_bad >= 0 and (first_conf < 0 or first_bad <= first_conf):
             raise InvalidWeightError(f"item {first_bad}: weight must be positive and finite, got {a_w[first_bad]}")
-        if first_conf is not None:
-            raise InconsistentWeightError(f"item {first_conf}: element {int(a_ids[first_conf])} reappeared with another weight")
-    y, s, _ = sketch_elements(a_ids, a_w, k, scheme)
+        if check and first_conf >= 0:
+            raise InconsistentWeightError(
+                f"item {first_conf}: element {int(a_ids[first_conf])} reappeared with another weight")
+        if skip_duplicates:
+            ids_t, w_t = ui[:n_uniq], uw[:n_uniq]
+    y, s, _ = sketch_elements(ids_t, w_t, k, scheme)
     y, s = y.cpu().numpy(), s.cpu().numpy().view(np.uint64)
     if exact_y:  # only the winners' (id, weight) pairs are scanned by the host walk
         keep = np.isin(a_ids, np.unique(s))

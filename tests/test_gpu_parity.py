@@ -384,6 +384,62 @@ def test_errors_map_to_reference_classes():
     assert sk.s == (1, 1, 1, 1)
 
 
+def _first_offenders(ids, w):
+    """stream_update's rules, item by item (stream.py:58-78)."""
+    seen = {}
+    bad = conf = -1
+    for i, (e, x) in enumerate(zip(ids.tolist(), w.tolist())):
+        if bad < 0 and not (math.isfinite(x) and x > 0 and x >= 1e-300):
+            bad = i
+        if e in seen:
+            if conf < 0 and seen[e] != x:
+                conf = i
+        else:
+            seen[e] = x
+    return bad, conf, seen
+
+
+def test_device_stream_checks_match_item_by_item_rules():
+    rng = np.random.default_rng(11)
+    for trial in range(6):
+        n = 20000
+        ids = rng.integers(0, 3000, n).astype(np.uint64)
+        ids[::997] = U64  # the table's empty-key value is a legal id
+        key_w = rng.exponential(1.0, 3000) + 0.01
+        w = np.where(ids == U64, 2.5, key_w[np.minimum(ids, 2999).astype(np.int64)])
+        if trial % 3 == 1:
+            w[rng.integers(100, n)] *= 1.5  # an inconsistent reappearance (or a first occurrence)
+        if trial % 3 == 2:
+            w[rng.integers(100, n)] = -1.0
+        bad, conf, seen = _first_offenders(ids, w)
+        dev_ids = torch.from_numpy(ids.view(np.int64)).cuda()
+        dev_w = torch.from_numpy(w).cuda()
+        ui, uw = torch.empty_like(dev_ids), torch.empty_like(dev_w)
+        out = np.zeros(3, np.int64)
+        rc = gm._lib.load().gm_check_pairs(dev_ids.data_ptr(), 64, dev_w.data_ptr(), 64, n, out[0:].ctypes.data,
+                                           out[1:].ctypes.data, ui.data_ptr(), uw.data_ptr(), out[2:].ctypes.data,
+                                           torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+        assert (int(out[0]), int(out[1])) == (bad, conf)
+        got = dict(zip(ui[: out[2]].cpu().numpy().view(np.uint64).tolist(), uw[: out[2]].cpu().tolist()))
+        assert got == seen  # first occurrences, with their weights
+
+
+def test_sketch_pairs_config4_prefix_bit_exact():
+    ids, w, k, seed = workloads.config4(n_pairs=1_000_000, n_keys=10**6)
+    sk = gm.sketch_pairs(ids, w, k, gm.SeedScheme(seed))
+    rc, yo, so, _, _ = O.sketch_stream(ids, w.astype(np.float64), k, seed)
+    assert rc == 0
+    assert np.array_equal(np.array(sk.s, np.uint64), so) and list(sk.y) == yo.tolist()
+    _, first_idx, inv = np.unique(ids, return_index=True, return_inverse=True)
+    rep = np.nonzero(first_idx[inv] < np.arange(ids.size))[0]
+    i = int(rep[len(rep) // 2])
+    bad = w.copy()
+    bad[i] *= 2  # a repeated id comes back with another weight
+    with pytest.raises(gm.InconsistentWeightError, match=f"item {i}:"):
+        gm.sketch_pairs(ids, bad, k, gm.SeedScheme(seed))
+
+
 def test_stream_state_api():
     sc = gm.SeedScheme(77)
     st = gm.StreamSketchState(2, sc)
