@@ -140,6 +140,13 @@ int gm_merge(const double *y_in, const uint64_t *s_in, int64_t n_sk,
 int gm_match_count(const uint64_t *s_a, const uint64_t *s_b, int64_t n_pairs,
                    int32_t k, int32_t *matches, void *stream);
 
+/* Cardinality estimates of n_sk sketches (estimate.py:90-100): sum_out[i] =
+ * the correctly rounded sum of y[i*k .. i*k+k) (== math.fsum), card_out[i]
+ * (nullable) = (k - 1) / sum_out[i].  Device arrays; asynchronous.  The
+ * caller raises InvalidParameterError for k < 2 as the reference does. */
+int gm_cardinality(const double *y, int64_t n_sk, int32_t k, double *sum_out,
+                   double *card_out, void *stream);
+
 /* K0 test surface (device arrays of length n): uniform_open
  * (randgen.py:107-119) and the permutation draw j in [z, k]
  * (rand_int_between(scheme, e, z, z, k), randgen.py:122-143). */

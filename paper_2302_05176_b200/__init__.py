@@ -30,6 +30,7 @@ from .estimate import (
     estimate_difference,
     estimate_jaccard_p,
     estimate_jaccard_p_batch,
+    estimate_cardinality_batch,
     estimate_set_algebra,
     exact_jaccard_p,
     exact_jaccard_w,

@@ -45,6 +45,7 @@ SIGNATURES = {
     "gm_sketch_elements_host": (_int, [_vp, _int, _vp, _int, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),
     "gm_merge": (_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp]),
     "gm_match_count": (_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
+    "gm_cardinality": (_int, [_vp, _i64, _i32, _vp, _vp, _vp]),
     "gm_uniform_open_batch": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "gm_perm_draw_batch": (_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "gm_arith_check": (_int, [_i64, _u64, _vp, _vp]),

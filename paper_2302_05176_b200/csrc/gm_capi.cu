@@ -702,6 +702,16 @@ int gm_match_count(const uint64_t* s_a, const uint64_t* s_b, int64_t n_pairs, in
   return GM_OK;
 }
 
+int gm_cardinality(const double* y, int64_t n_sk, int32_t k, double* sum_out, double* card_out, void* stream) {
+  g_msg[0] = 0;
+  (void)cudaGetLastError();
+  if (k < 1) return fail(GM_ERR_INVALID_PARAMETER, "k must be >= 1");
+  if (n_sk <= 0) return GM_OK;
+  exact_sum_kernel<<<(unsigned)n_sk, 256, 0, (cudaStream_t)stream>>>(y, n_sk, (u32)k, sum_out, card_out);
+  CK(cudaGetLastError());
+  return GM_OK;
+}
+
 int gm_uniform_open_batch(const uint64_t* global_seeds, const uint64_t* elements,
                           const uint64_t* steps, int64_t n, double* out, void* stream) {
   g_msg[0] = 0;

@@ -257,6 +257,87 @@ __global__ void match_count_kernel(const u64* __restrict__ s_a, const u64* __res
   }
 }
 
+// ---- estimators: exactly rounded register sums (math.fsum, estimate.py:100)
+// One CTA per sketch.  Every y >= 0 is m * 2^e with a 53-bit integer m; it
+// is added exactly into a fixed-point superaccumulator of 32-bit digits
+// (int64 limbs in shared memory absorb the carries of up to 2^31 adds), the
+// carries are propagated once, and the top digits are rounded to nearest
+// even with a sticky bit: the correctly rounded sum, i.e. math.fsum's.
+// card = (k - 1) / sum (an IEEE divide, like the reference's).  A +inf
+// register gives +inf (card 0); a negative or NaN one gives NaN.
+constexpr int SUM_DIGITS = 68;  // 32 * 68 bits >= 1074 + 1024 + 53 + carry room
+
+__global__ void __launch_bounds__(256) exact_sum_kernel(const double* __restrict__ y, int64_t n_sk, u32 k,
+                                                        double* __restrict__ sum_out,
+                                                        double* __restrict__ card_out) {
+  __shared__ unsigned long long acc[SUM_DIGITS];
+  __shared__ int special;  // bit 0: +inf seen, bit 1: NaN / negative seen
+  const int64_t sk = blockIdx.x;
+  if (sk >= n_sk) return;
+  for (int i = threadIdx.x; i < SUM_DIGITS; i += blockDim.x) acc[i] = 0;
+  if (threadIdx.x == 0) special = 0;
+  __syncthreads();
+  for (u32 j = threadIdx.x; j < k; j += blockDim.x) {
+    const double v = y[sk * (int64_t)k + j];
+    const u64 b = (u64)__double_as_longlong(v);
+    const int ex = (int)((b >> 52) & 0x7FF);
+    if ((b >> 63) && v != 0.0) { atomicOr(&special, 2); continue; }
+    if (ex == 0x7FF) { atomicOr(&special, (b & 0xFFFFFFFFFFFFFull) ? 2 : 1); continue; }
+    const u64 m = (b & 0xFFFFFFFFFFFFFull) | (ex ? (1ull << 52) : 0ull);
+    if (!m) continue;
+    const int p = ex ? ex - 1 : 0;  // bit position of m's lsb above 2^-1074
+    const unsigned __int128 sh = (unsigned __int128)m << (p & 31);
+    const int q = p >> 5;
+    atomicAdd(&acc[q], (unsigned long long)(u32)sh);
+    atomicAdd(&acc[q + 1], (unsigned long long)(u32)(sh >> 32));
+    atomicAdd(&acc[q + 2], (unsigned long long)(u32)(sh >> 64));
+  }
+  __syncthreads();
+  if (threadIdx.x) return;
+  double total;
+  if (special & 2) {
+    total = __longlong_as_double(0x7FF8000000000000ll);
+  } else if (special & 1) {
+    total = __longlong_as_double(0x7FF0000000000000ll);
+  } else {
+    unsigned long long carry = 0;
+    int top = -1;
+    for (int i = 0; i < SUM_DIGITS; ++i) {
+      const unsigned long long t = acc[i] + carry;
+      acc[i] = t & 0xFFFFFFFFull;
+      carry = t >> 32;
+      if (acc[i]) top = i;
+    }
+    if (top < 0) {
+      total = 0.0;
+    } else {
+      // the top three digits as a 96-bit integer, the rest as a sticky bit
+      unsigned __int128 mant = 0;
+      bool sticky = false;
+      const int lo = top >= 2 ? top - 2 : 0;
+      for (int i = top; i >= lo; --i) mant = (mant << 32) | acc[i];
+      for (int i = lo - 1; i >= 0; --i) sticky |= acc[i] != 0;
+      const int msb = 127 - (mant >> 64 ? __clzll((long long)(u64)(mant >> 64)) : 64 + __clzll((long long)(u64)mant));
+      int e = 32 * lo - 1074;  // weight of mant's lsb
+      u64 r;
+      if (msb > 52) {
+        const int shift = msb - 52;
+        r = (u64)(mant >> shift);
+        const unsigned __int128 rem = mant & (((unsigned __int128)1 << shift) - 1);
+        const unsigned __int128 half = (unsigned __int128)1 << (shift - 1);
+        if (rem > half || (rem == half && (sticky || (r & 1)))) ++r;
+        e += shift;
+        if (r >> 53) { r >>= 1; ++e; }
+      } else {
+        r = (u64)mant;  // exact: fewer than 54 significant bits and no lower digits
+      }
+      total = scalbn((double)r, e);  // exact for the normal sums registers produce
+    }
+  }
+  sum_out[sk] = total;
+  if (card_out) card_out[sk] = __ddiv_rn((double)(k - 1), total);
+}
+
 // ---- K0 test kernels: the keyed streams element by element ----
 __global__ void uniform_kernel(const u64* seeds, const u64* elems, const u64* steps, int64_t n,
                                double* out) {

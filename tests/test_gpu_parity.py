@@ -384,6 +384,30 @@ def test_errors_map_to_reference_classes():
     assert sk.s == (1, 1, 1, 1)
 
 
+def test_device_register_sum_is_fsum():
+    """gm_cardinality: exactly rounded sums (math.fsum) and (k-1)/sum."""
+    rng = np.random.default_rng(21)
+    rows = [rng.exponential(1e-3, 1024),
+            np.exp(rng.uniform(-700, 700, 1024)),                  # 600 decades in one sum
+            np.concatenate([[1.0], np.full(1023, 2.0**-60)]),      # ties and sticky bits
+            np.concatenate([[2.0**53], np.ones(1023)]),
+            np.full(1024, 5e-324),                                 # subnormals
+            np.zeros(1024),
+            rng.random(1024) * np.where(rng.random(1024) < 0.5, 1e-200, 1e200)]
+    y = torch.from_numpy(np.stack(rows)).cuda()
+    sums = torch.empty(len(rows), dtype=torch.float64, device="cuda")
+    card = torch.empty_like(sums)
+    assert gm._lib.load().gm_cardinality(y.data_ptr(), len(rows), 1024, sums.data_ptr(), card.data_ptr(),
+                                         torch.cuda.current_stream().cuda_stream) == 0
+    got = sums.cpu().tolist()
+    for r, g in zip(rows, got):
+        assert g == math.fsum(r.tolist())
+    ids, w, off, k, seed = workloads.config2(n_vectors=64)
+    b = gm.sketch_csr(ids, w, off, k, gm.SeedScheme(seed))
+    c = gm.estimate_cardinality_batch(b).cpu().tolist()
+    assert c == [gm.estimate_cardinality(sk).value for sk in b.to_sketches()]
+
+
 def _first_offenders(ids, w):
     """stream_update's rules, item by item (stream.py:58-78)."""
     seen = {}
