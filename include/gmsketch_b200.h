@@ -201,6 +201,11 @@ int gm_exact_y(const void *ids, int id_bits, const void *w, int w_bits,
 /* Work counters of a library built with -DGM_STATS (tools/stats.py): copies
  * and clears 16 u64 host words; GM_ERR_INVALID_PARAMETER in normal builds. */
 int gm_stats_read(unsigned long long *out16);
+/* Slot events of a -DGM_EVENTS build (tools/timeline.py): ev_out up to
+ * 32768 x 2 u64 (globaltimer ns, vector | pass << 32 | kind << 40 | cta << 48
+ * | slot << 60; kind 0 load, 1 written, 2 re-opened), *n_out their count;
+ * clears them.  GM_ERR_INVALID_PARAMETER in normal builds. */
+int gm_trace_read(unsigned long long *ev_out, unsigned *n_out);
 
 /* Diagnostics.
  * gm_probe_arrival_rate: n_threads threads each emit `iters` exact arrivals

@@ -38,6 +38,7 @@ SIGNATURES = {
     "gm_debug_error": (_int, [_vp]),
     "gm_last_error": (ctypes.c_char_p, []),
     "gm_stats_read": (_int, [_vp]),
+    "gm_trace_read": (_int, [_vp, _vp]),
     "gm_stream_status": (_int, [_vp]),
     "gm_sketch_csr": (_int, [_vp, _int, _vp, _int, _vp, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),
     "gm_sketch_csr_host": (_int, [_vp, _int, _vp, _int, _vp, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),

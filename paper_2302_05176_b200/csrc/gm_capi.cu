@@ -456,6 +456,26 @@ int gm_check_pairs(const void* ids, int id_bits, const void* w, int w_bits, int6
   return GM_OK;
 }
 
+// -DGM_EVENTS builds only (tools/timeline.py): slot events (n x 2 u64, up
+// to 32768) and their count; clears them
+int gm_trace_read(unsigned long long* ev_out, unsigned* n_out) {
+#ifdef GM_EVENTS
+  CK(cudaDeviceSynchronize());
+  unsigned n = 0;
+  CK(cudaMemcpyFromSymbol(&n, g_trace_n, sizeof(n)));
+  if (n > 32768) n = 32768;
+  if (n) CK(cudaMemcpyFromSymbol(ev_out, g_trace, sizeof(unsigned long long) * 2 * n));
+  *n_out = n;
+  unsigned zn = 0;
+  CK(cudaMemcpyToSymbol(g_trace_n, &zn, sizeof(zn)));
+  return GM_OK;
+#else
+  (void)ev_out;
+  (void)n_out;
+  return fail(GM_ERR_INVALID_PARAMETER, "library built without GM_EVENTS");
+#endif
+}
+
 int gm_stream_status(void* stream) {
   Workspace* ws = nullptr;
   int rc = get_ws((cudaStream_t)stream, &ws);

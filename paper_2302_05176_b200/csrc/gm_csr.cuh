@@ -459,6 +459,8 @@ __device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const
       sl.emitted = 0;
       sl.seq = ++S.seq;
       slot_open_pass(sl, k, attempt0, C::kDeep);
+      GM_TRACE((unsigned long long)(v & 0xFFFFFFFF) | ((unsigned long long)attempt0 << 32) |
+               ((unsigned long long)blockIdx.x << 48) | ((unsigned long long)s << 60));
     }
     __syncwarp();
     return;
@@ -598,7 +600,11 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       for (u32 j = lane; j < k; j += 32) unset |= regs[j].y == INF_BITS;
       const int att = __shfl_sync(FULL, *(volatile int*)&sl.attempt, 0);
       if (__any_sync(FULL, unset) && att < 3) {
-        if (lane == 0) slot_open_pass(sl, k, att + 1, C::kDeep);
+        if (lane == 0) {
+          slot_open_pass(sl, k, att + 1, C::kDeep);
+          GM_TRACE((unsigned long long)(sl.v & 0xFFFFFFFF) | ((unsigned long long)(att + 1) << 32) | (2ull << 40) |
+                   ((unsigned long long)blockIdx.x << 48) | ((unsigned long long)s << 60));
+        }
         __syncwarp();
         continue;
       }
@@ -609,6 +615,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         s_out[v * (int64_t)k + j] = rg.id;
       }
       if (emitted_out && lane == 0) emitted_out[v] = (int64_t)sl.emitted;
+      if (lane == 0)
+        GM_TRACE((unsigned long long)(v & 0xFFFFFFFF) | ((unsigned long long)att << 32) | (1ull << 40) |
+                 ((unsigned long long)blockIdx.x << 48) | ((unsigned long long)s << 60));
       __syncwarp();
       slot_load<C>(S, s, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list);
     }
