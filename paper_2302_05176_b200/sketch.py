@@ -206,7 +206,7 @@ def sketch_csr(ids, weights, offsets, k: int, scheme: SeedScheme, *, exhaustive:
     weights: float32/float64; offsets: int64 [n_vec + 1].  Ids must be
     distinct within a vector (WeightedVector keys).  Device tensors are used
     in place; host arrays are copied in.  ``split=True`` selects the
-    experimental split schedule (DESIGN.md §6.2); results are identical.
+    experimental split schedule (DESIGN.md §6.3); results are identical.
     ``exact_y=True`` re-derives y on the host with the reference's
     arithmetic (exact_y_host): bit-identical y, at host cost."""
     _check_k(k)
