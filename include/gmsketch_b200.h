@@ -90,7 +90,11 @@ int gm_sketch_csr(const void *ids, int id_bits, const void *w, int w_bits,
                   double *y_out, uint64_t *s_out, int64_t *emitted_out,
                   void *stream);
 
-/* Same contract with HOST buffers; copies in and out inside the call. */
+/* Same contract with HOST buffers; copies in and out inside the call (page-
+ * locked outputs are stored by the kernel directly).  With GM_FLAG_ASYNC the
+ * call only enqueues: the caller keeps the buffers untouched until `stream`
+ * is synchronised.  Alternating two streams pipelines batches: one batch's
+ * input copy and first CTAs overlap the previous batch's tail. */
 int gm_sketch_csr_host(const void *ids, int id_bits, const void *w, int w_bits,
                        const int64_t *offsets, int64_t n_vec, int32_t k,
                        uint64_t global_seed, uint64_t stream_salt,

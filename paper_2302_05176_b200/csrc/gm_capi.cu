@@ -628,6 +628,9 @@ int gm_sketch_csr_host(const void* ids, int id_bits, const void* w, int w_bits,
     CK(cudaMemcpyAsync(s_out, d_s, yb, cudaMemcpyDeviceToHost, st));
     if (d_em) CK(cudaMemcpyAsync(emitted_out, d_em, (size_t)n_vec * 8, cudaMemcpyDeviceToHost, st));
   }
+  // GM_FLAG_ASYNC: enqueue only (inputs and outputs stay in use until the
+  // stream is synchronised; data errors via gm_stream_status)
+  if (flags & GM_FLAG_ASYNC) return GM_OK;
   return check_sync(ws, st);
 }
 
