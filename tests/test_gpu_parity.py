@@ -318,6 +318,40 @@ def test_host_api_matches_device_api():
     assert np.array_equal(s2, s)
 
 
+def test_batches_pipelined_over_streams():
+    """GM_FLAG_ASYNC calls on alternating streams (the bench's stream of
+    batches), device and host entry points: every batch equals the
+    synchronous result."""
+    ids, w, off, k, seed = workloads.config2(n_vectors=300)
+    sc = gm.SeedScheme(seed)
+    ref = gm.sketch_csr(ids, w, off, k, sc)
+    L = gm._lib.load()
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    n_vec = len(off) - 1
+    d_ids = torch.from_numpy(ids.view(np.int32)).cuda()
+    d_w, d_off = torch.from_numpy(w).cuda(), torch.from_numpy(off).cuda()
+    ys = [torch.empty((n_vec, k), dtype=torch.float64, device="cuda") for _ in range(6)]
+    ss = [torch.empty((n_vec, k), dtype=torch.int64, device="cuda") for _ in range(6)]
+    h_ids = torch.from_numpy(ids.view(np.int32)).pin_memory()
+    h_w, h_off = torch.from_numpy(w).pin_memory(), torch.from_numpy(off).pin_memory()
+    hy = [torch.empty((n_vec, k), dtype=torch.float64).pin_memory() for _ in range(6)]
+    hs = [torch.empty((n_vec, k), dtype=torch.int64).pin_memory() for _ in range(6)]
+    torch.cuda.synchronize()
+    for i in range(6):
+        st = streams[i % 3].cuda_stream
+        assert L.gm_sketch_csr(d_ids.data_ptr(), 32, d_w.data_ptr(), 32, d_off.data_ptr(), n_vec, k, sc.global_seed,
+                               sc.stream_salt, gm._lib.GM_FLAG_ASYNC, ys[i].data_ptr(), ss[i].data_ptr(), 0, st) == 0
+        assert L.gm_sketch_csr_host(h_ids.data_ptr(), 32, h_w.data_ptr(), 32, h_off.data_ptr(), n_vec, k,
+                                    sc.global_seed, sc.stream_salt, gm._lib.GM_FLAG_ASYNC, hy[i].data_ptr(),
+                                    hs[i].data_ptr(), 0, st) == 0
+    torch.cuda.synchronize()
+    for st in streams:
+        assert L.gm_stream_status(st.cuda_stream) == 0
+    for i in range(6):
+        assert torch.equal(ss[i], ref.s) and torch.equal(ys[i], ref.y)
+        assert torch.equal(hs[i], ref.s.cpu()) and torch.equal(hy[i], ref.y.cpu())
+
+
 # ---------------------------------------------------------------- edge cases
 def test_single_element_owns_every_register():
     for k in (1, 3, 64, 1024, 4096):
