@@ -84,6 +84,8 @@ struct Workspace {
   size_t vsum_cap = 0;
   int* vflag = nullptr;                    // per-vector flags (CSR prep)
   size_t vflag_cap = 0;
+  int64_t* surv = nullptr;                 // K2 filter survivors
+  size_t surv_cap = 0;
   void* stage = nullptr;                   // device staging for *_host calls
   size_t stage_cap = 0;
   u64* pt_keys = nullptr;                  // gm_check_pairs id table
@@ -347,22 +349,50 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&light_per_sm, elem_light_kernel<IdT, WT>, NT, 0));
     int64_t lgrid = (int64_t)light_per_sm * num_sms();
     lgrid = std::min<int64_t>(lgrid, (n + NT - 1) / NT);
+    // filter pass (HBM-streaming first-arrival test, survivors compacted)
+    // for finite thresholds; the fused light kernel when tau is +inf, when
+    // the survivor list overflows, or with GM_ELEM_FUSED=1
+    static const bool fused_only = getenv("GM_ELEM_FUSED") && atoi(getenv("GM_ELEM_FUSED")) == 1;
+    const int64_t surv_cap = std::min<int64_t>(n, (int64_t)1 << 26);
+    if ((rc = grow(&ws->surv, &ws->surv_cap, (size_t)surv_cap, st))) return rc;
+    const int64_t fgrid = std::min<int64_t>((n / 4 + 2 * NT - 1) / (2 * NT) + 1, (int64_t)num_sms() * 8);
     for (int attempt = 0;; ++attempt) {
-      tau_kernel<<<1, 1, 0, st>>>(ws->dbl, ws->dbl + 1, k, (flags & GM_FLAG_EXHAUSTIVE) ? 5 : attempt,
-                                  ws->counters + 1);
+      const int att = (flags & GM_FLAG_EXHAUSTIVE) ? 5 : attempt;
+      tau_kernel<<<1, 1, 0, st>>>(ws->dbl, ws->dbl + 1, k, att, ws->counters + 1);
       CK(cudaMemsetAsync(ws->ull, 0, sizeof(unsigned long long), st));
-      elem_light_kernel<IdT, WT><<<(unsigned)lgrid, NT, 0, st>>>(
-          (const IdT*)ids, (const WT*)w, n, k, useed, pseed, ws->dbl, ws->regs, ws->counters + 1,
-          ws->heavy, (int64_t)ws->heavy_cap, ws->ull, emitted_out ? ws->ull + 1 : nullptr, ws->err);
-      CK(cudaGetLastError());
-      elem_heavy_kernel<IdT, WT><<<(unsigned)heavy_blocks, NT, 0, st>>>(
-          (const IdT*)ids, (const WT*)w, k, useed, pseed, ws->dbl, ws->regs, ws->counters + 1,
-          ws->heavy, ws->ull, (int64_t)ws->heavy_cap, ws->dense,
-          emitted_out ? ws->ull + 1 : nullptr);
-      CK(cudaGetLastError());
-      CK(cudaMemcpyAsync(ws->host, ws->counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(ws->host + 1, ws->ull, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
+      bool use_filter = !fused_only && att < 4;
+      for (int round = 0; round < 2; ++round) {
+        if (use_filter) {
+          CK(cudaMemsetAsync(ws->ull + 2, 0, sizeof(unsigned long long), st));
+          elem_filter_kernel<IdT, WT><<<(unsigned)fgrid, NT, 0, st>>>(
+              (const IdT*)ids, (const WT*)w, n, k, useed, ws->dbl, ws->surv, surv_cap, ws->ull + 2,
+              emitted_out ? ws->ull + 1 : nullptr, ws->err);
+          CK(cudaGetLastError());
+          elem_survivor_kernel<IdT, WT><<<(unsigned)(num_sms() * 4), NT, 0, st>>>(
+              (const IdT*)ids, (const WT*)w, ws->surv, ws->ull + 2, surv_cap, k, useed, pseed, ws->dbl, ws->regs,
+              ws->counters + 1, ws->heavy, (int64_t)ws->heavy_cap, ws->ull, emitted_out ? ws->ull + 1 : nullptr);
+        } else {
+          elem_light_kernel<IdT, WT><<<(unsigned)lgrid, NT, 0, st>>>(
+              (const IdT*)ids, (const WT*)w, n, k, useed, pseed, ws->dbl, ws->regs, ws->counters + 1,
+              ws->heavy, (int64_t)ws->heavy_cap, ws->ull, emitted_out ? ws->ull + 1 : nullptr, ws->err);
+        }
+        CK(cudaGetLastError());
+        elem_heavy_kernel<IdT, WT><<<(unsigned)heavy_blocks, NT, 0, st>>>(
+            (const IdT*)ids, (const WT*)w, k, useed, pseed, ws->dbl, ws->regs, ws->counters + 1,
+            ws->heavy, ws->ull, (int64_t)ws->heavy_cap, ws->dense,
+            emitted_out ? ws->ull + 1 : nullptr);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(ws->host, ws->counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ws->host + 1, ws->ull, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ws->host + 3, ws->ull + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (use_filter && (int64_t)ws->host[3] > surv_cap) {  // list overflow: redo the pass fused (idempotent)
+          use_filter = false;
+          CK(cudaMemsetAsync(ws->ull, 0, sizeof(unsigned long long), st));
+          continue;
+        }
+        break;
+      }
       const int unset = (int)(ws->host[0] & 0xFFFFFFFFull);
       const unsigned long long nheavy = ws->host[1];
       if (nheavy > ws->heavy_cap)

@@ -118,6 +118,194 @@ __global__ void __launch_bounds__(NT)
   }
 }
 
+// ---- K2 filter pass: stream the element arrays once at HBM speed --------
+// Every element's first arrival is tested with an fp32 bound (no fp64, no
+// log): u1 = (h >> 11) 2^-53 + 2^-54 < ((h >> 40) + 1) 2^-24, and the element
+// is skipped when ((h >> 40) + 1) < 2^24 (1 - 2^-12) exp(-tau k w), the right
+// side taken as ex2.approx(fma(x, -log2 e, 23.9996)) (24 + log2(1 - 2.8e-4)) with
+// x = tau k w in fp32.  Error budget: the fp32 roundings of tau k and x move
+// the exponent by <= 104 * 2^-23 (beyond 104 the threshold is 0 and nothing
+// is skipped), the fma by <= 150 * 2^-24, ex2.approx by ~2^-22 -- together
+// < 2^-15, well inside the 2.8e-4 margin, so an element is skipped only if its
+// exact fp64 first arrival exceeds tau.  Only bits 40..63 of the hash are
+// needed, and mix64's final xor-shift leaves them unchanged.  The few
+// survivors (~k (ln k + c) per pass) are compacted into a list for the walk
+// kernel; u32 ids with fp32 weights are read as uint4/float4.
+__device__ __forceinline__ u32 mix64_hi24(u64 x) {
+  x = (x ^ (x >> 30)) * M1;
+  x = x ^ (x >> 27);
+  return (u32)((x * M2) >> 40);
+}
+
+__device__ __forceinline__ bool filter_skip_f(u64 ubase, float x) {
+  float thr;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(thr) : "f"(__fmaf_rn(x, -1.4426950408889634f, 23.9996f)));
+  return (float)(mix64_hi24(ubase + K_STEP) + 1u) < thr;
+}
+
+template <class WT>
+__device__ __forceinline__ bool weight_ok_t(WT w) {
+  if (sizeof(WT) == 4) {
+    const float f = (float)w;
+    return f > 0.0f && f < __int_as_float(0x7F800000);  // any positive finite float is >= 1e-300
+  }
+  return weight_ok((double)w);
+}
+
+template <class WT>
+__device__ __forceinline__ float filter_x(WT w, float tkf, double tk) {
+  return sizeof(WT) == 4 ? tkf * (float)w : (float)(tk * (double)w);
+}
+
+// Survivor ids already listed by this CTA in this pass: a repeated id (a
+// stream duplicate: same weight, hence the same arrivals) is a register
+// no-op, so it is listed once per CTA instead of once per occurrence (Zipf
+// streams repeat their hot keys millions of times).  Open addressing, 8
+// probes, then it is simply listed again.
+constexpr int SURV_CACHE = 1024;
+
+__device__ __forceinline__ bool surv_cache_first(unsigned long long* cache, u64 id) {
+  u32 h = (u32)(mix64(id ^ 0x2545F4914F6CDD1Dull) >> 32) & (SURV_CACHE - 1);
+  for (int p = 0; p < 8; ++p) {
+    const unsigned long long prev = atomicCAS(&cache[h], ~0ull, (unsigned long long)id);
+    if (prev == ~0ull) return true;   // inserted: first occurrence here
+    if (prev == (unsigned long long)id) return false;
+    h = (h + 1) & (SURV_CACHE - 1);
+  }
+  return true;
+}
+
+// rare path: append the flagged elements (bit e of keep = element base + e * step)
+template <class IdT>
+__device__ __noinline__ void append_flagged(u32 keep, u32 bad, int64_t base, int64_t step, int nbits, int64_t* list,
+                                            int64_t cap, unsigned long long* count, unsigned long long* err,
+                                            const IdT* ids, unsigned long long* cache) {
+  const int lane = threadIdx.x & 31;
+  for (int e = 0; e < nbits; ++e) {
+    bool kp = (keep >> e) & 1u;
+    if (kp) kp = surv_cache_first(cache, (u64)ids[base + e * step]);
+    if ((bad >> e) & 1u) raise_error(err, 2u, (u64)(base + e * step));
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, kp);
+    if (!m) continue;
+    unsigned long long b = 0;
+    if (lane == __ffs(m) - 1) b = atomicAdd(count, (unsigned long long)__popc(m));
+    b = __shfl_sync(0xFFFFFFFFu, b, __ffs(m) - 1);
+    if (kp) {
+      const unsigned long long pos = b + __popc(m & ((1u << lane) - 1u));
+      if ((int64_t)pos < cap) list[pos] = base + e * step;
+    }
+  }
+}
+
+template <class IdT, class WT>
+__global__ void __launch_bounds__(NT)
+    elem_filter_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, int64_t n, u32 k, u64 useed,
+                       const double* __restrict__ tau_p, int64_t* __restrict__ list, int64_t cap,
+                       unsigned long long* count, unsigned long long* emitted_total, unsigned long long* err) {
+  __shared__ unsigned long long cache[SURV_CACHE];
+  for (int i = threadIdx.x; i < SURV_CACHE; i += NT) cache[i] = ~0ull;
+  __syncthreads();
+  const double tk = *tau_p * (double)k;
+  const float tkf = (float)tk;
+  u32 skipped = 0;
+  constexpr bool kVec = sizeof(WT) == 4;  // fp32 weights: float4; ids uint4 (u32) or 2 x ulonglong2 (u64)
+  const int64_t tid = (int64_t)blockIdx.x * NT + threadIdx.x, nthr = (int64_t)gridDim.x * NT;
+  const bool vec = kVec && (((uintptr_t)ids | (uintptr_t)wts) & 15) == 0;
+  int64_t first = 0;
+  if (vec) {
+    const int64_t nq = n >> 2;  // quads
+    const float4* wq = reinterpret_cast<const float4*>(wts);
+    // full rounds: every thread has two quads (warp-uniform trip count)
+    const int64_t rounds = nq / (2 * nthr);
+    for (int64_t r = 0; r < rounds; ++r) {
+      const int64_t q0 = r * 2 * nthr + tid, q1 = q0 + nthr;
+      u64 idv[8];
+      if (sizeof(IdT) == 4) {
+        const uint4* iq = reinterpret_cast<const uint4*>(ids);
+        const uint4 i0 = __ldcs(&iq[q0]), i1 = __ldcs(&iq[q1]);
+        idv[0] = i0.x; idv[1] = i0.y; idv[2] = i0.z; idv[3] = i0.w;
+        idv[4] = i1.x; idv[5] = i1.y; idv[6] = i1.z; idv[7] = i1.w;
+      } else {
+        const ulonglong2* iq = reinterpret_cast<const ulonglong2*>(ids);
+        const ulonglong2 a0 = __ldcs(&iq[2 * q0]), a1 = __ldcs(&iq[2 * q0 + 1]);
+        const ulonglong2 b0 = __ldcs(&iq[2 * q1]), b1 = __ldcs(&iq[2 * q1 + 1]);
+        idv[0] = a0.x; idv[1] = a0.y; idv[2] = a1.x; idv[3] = a1.y;
+        idv[4] = b0.x; idv[5] = b0.y; idv[6] = b1.x; idv[7] = b1.y;
+      }
+      const float4 w0 = __ldcs(&wq[q0]), w1 = __ldcs(&wq[q1]);
+      const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+      u32 keep = 0, bad = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const bool ok = weight_ok_t(wv[e]);
+        const bool sk = filter_skip_f(useed + idv[e] * K_ELEM, tkf * wv[e]);
+        bad |= (u32)!ok << e;
+        keep |= (u32)(ok && !sk) << e;
+        skipped += ok && sk;
+      }
+      if (__any_sync(0xFFFFFFFFu, (keep | bad) != 0u)) {
+        // bit e: quad q0 (e < 4) or q1 (e >= 4), element e & 3
+        append_flagged(keep & 15u, bad & 15u, 4 * q0, 1, 4, list, cap, count, err, ids, cache);
+        append_flagged(keep >> 4, bad >> 4, 4 * q1, 1, 4, list, cap, count, err, ids, cache);
+      }
+    }
+    first = rounds * 2 * nthr * 4;
+  }
+  // scalar path: everything (no vector loads) or what the full rounds left
+  for (int64_t i0 = first + tid; i0 - tid < n; i0 += nthr) {
+    u32 keep = 0, bad = 0;
+    if (i0 < n) {
+      const WT w = __ldcs(&wts[i0]);
+      const bool ok = weight_ok_t(w);
+      const bool sk = ok && filter_skip_f(useed + (u64)__ldcs(&ids[i0]) * K_ELEM, filter_x(w, tkf, tk));
+      bad = !ok;
+      keep = ok && !sk;
+      skipped += sk;
+    }
+    if (__any_sync(0xFFFFFFFFu, (keep | bad) != 0u))
+      append_flagged(keep, bad, i0, 1, 1, list, cap, count, err, ids, cache);
+  }
+  if (emitted_total) {
+    unsigned long long e = skipped;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xFFFFFFFFu, e, o);
+    if ((threadIdx.x & 31) == 0 && e) atomicAdd(emitted_total, e);
+  }
+}
+
+// survivors of the filter: walk light elements lane-parallel (as the fused
+// light kernel does); heavy or table-full ones go to the heavy list
+template <class IdT, class WT>
+__global__ void __launch_bounds__(NT)
+    elem_survivor_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, const int64_t* __restrict__ list,
+                         const unsigned long long* count, int64_t cap, u32 k, u64 useed, u64 pseed,
+                         const double* __restrict__ tau_p, Reg* regs, int* unset_ctr, u64* __restrict__ heavy_list,
+                         int64_t heavy_cap, unsigned long long* heavy_count, unsigned long long* emitted_total) {
+  __shared__ u32 maps[16 * NT];
+  const double tau = *tau_p;
+  const double light_w = 8.0 / ((double)k * tau);
+  const int64_t m = min((int64_t)*count, cap);
+  u32 emitted = 0;
+  u32* mymap = maps + threadIdx.x;
+  for (int64_t j = (int64_t)blockIdx.x * NT + threadIdx.x; j < m; j += (int64_t)gridDim.x * NT) {
+    const int64_t i = list[j];
+    const double w = load_w(wts, i);
+    const u64 id = load_id(ids, i);
+    bool ok = false;
+    if (w < light_w) ok = walk_light<false>(id, w, tau, k, useed, pseed, mymap, NT, 16, regs, unset_ctr, emitted);
+    if (!ok) {
+      const unsigned long long h = atomicAdd(heavy_count, 1ull);
+      if ((int64_t)h < heavy_cap) heavy_list[h] = (u64)i;
+    }
+  }
+  if (emitted_total) {
+    unsigned long long e = emitted;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xFFFFFFFFu, e, o);
+    if ((threadIdx.x & 31) == 0 && e) atomicAdd(emitted_total, e);
+  }
+}
+
 // one warp per heavy element; dense arrays in global scratch, one per warp
 template <class IdT, class WT>
 __global__ void __launch_bounds__(NT)
