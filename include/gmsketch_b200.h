@@ -186,6 +186,17 @@ int gm_check_pairs(const void *ids, int id_bits, const void *w, int w_bits,
                    void *uniq_ids, void *uniq_w, int64_t *n_uniq,
                    void *stream);
 
+/* One element queue advanced on the host (ElementQueueState /
+ * next_order_statistic, randgen.py:210-271, over _run_queue :158-207):
+ * emissions z0+1 .. z0+steps of `element` (weight w, k servers) from running
+ * time b0; perm (host, k entries: the Fisher-Yates array, values 1..k) is
+ * updated in place; t_out[i], s_out[i] = emitted time and server.  glibc log,
+ * the reference's operation order.  Host memory only; no CUDA. */
+int gm_queue_advance(uint64_t global_seed, uint64_t stream_salt,
+                     uint64_t element, double w, int32_t k, int32_t z0,
+                     int32_t steps, double b0, uint32_t *perm, double *t_out,
+                     uint32_t *s_out);
+
 /* Exact-y finalize (host memory only; no CUDA): y_io[v*k + j] := the
  * arrival time the reference computes for register j of CSR vector v,
  * given its winning element s[v*k + j] (from gm_sketch_csr* /

@@ -39,10 +39,12 @@ from .estimate import (
 )
 from .randgen import (
     DEFAULT_STREAM_SALT,
+    ElementQueueState,
     LazyPermutation,
     SeedScheme,
     derive_seed,
     mix64,
+    next_order_statistic,
     perm_draw_batch,
     rand_int_between,
     uniform_open,

@@ -10,6 +10,7 @@ reference.
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -124,3 +125,51 @@ def rand_int_between(scheme: SeedScheme, element: int, step: int, lo: int, hi: i
     # the device draw is z + (g mod m) with m = k - z + 1; key is (element, step)
     j = perm_draw_batch([scheme.perm_seed], [element], [step], [step + m - 1])[0]
     return lo + int(j) - step
+
+
+class ElementQueueState:
+    """Generation cursor for one element's queue of k customers
+    (randgen.py:210-242): emitted count z, last emitted value b, and the
+    Fisher-Yates array perm (values 1..k).  Advanced on the host by
+    gm_queue_advance with the reference's arithmetic (this is the
+    reference's one-emission-at-a-time API surface; the sketch kernels never
+    use it)."""
+
+    def __init__(self, element_id: int, weight: float, k: int, z: int = 0, b: float = 0.0, perm=None):
+        from .errors import InvalidWeightError
+
+        weight = float(weight)
+        if not (weight > 0.0) or not math.isfinite(weight):
+            raise InvalidWeightError(f"element {element_id}: weight must be positive and finite, got {weight}")
+        if weight < MIN_WEIGHT:
+            raise InvalidWeightError(f"element {element_id}: weight {weight} below {MIN_WEIGHT}")
+        self.element_id = int(element_id)
+        self.weight = weight
+        self.k = int(k)
+        self.z = int(z)
+        self.b = float(b)
+        self.perm = (np.arange(1, self.k + 1, dtype=np.uint32) if perm is None or len(perm) == 0
+                     else np.ascontiguousarray(np.asarray(perm, dtype=np.uint32)))
+
+    @property
+    def exhausted(self) -> bool:
+        return self.z >= self.k
+
+
+def next_order_statistic(state: ElementQueueState, scheme: SeedScheme) -> tuple[float, int]:
+    """Advance a queue by one emission; (arrival time, server) (randgen.py:245-271)."""
+    from . import _lib
+    from .errors import QueueExhaustedError
+
+    if state.z >= state.k:
+        raise QueueExhaustedError(f"element {state.element_id}: all {state.k} order statistics emitted")
+    t = np.zeros(1, np.float64)
+    srv = np.zeros(1, np.uint32)
+    rc = _lib.load().gm_queue_advance(scheme.global_seed, scheme.stream_salt, state.element_id & MASK64,
+                                      state.weight, state.k, state.z, 1, state.b, state.perm.ctypes.data,
+                                      t.ctypes.data, srv.ctypes.data)
+    if rc:
+        raise ValueError(f"gm_queue_advance failed ({rc})")
+    state.z += 1
+    state.b = float(t[0])
+    return state.b, int(srv[0])

@@ -58,3 +58,23 @@ def test_foreign_winner_is_rejected():
     with pytest.raises(gm.MismatchedSketchError):
         gm.exact_y_host(ids, w, np.array([0, ids.size]), case["k"], gm.SeedScheme(case["seed"]), ws,
                         np.zeros(case["k"]))
+
+
+def test_element_queue_state_matches_reference_queues():
+    """ElementQueueState / next_order_statistic (host, gm_queue_advance) against
+    the reference's full queues (tests/golden/rng_kats.json): bit-identical
+    times and servers; QueueExhaustedError after k; weight validation."""
+    for q in load_json("rng_kats.json")["queues"]:
+        sc = gm.SeedScheme(q["seed"])
+        st = gm.ElementQueueState(q["element"], float.fromhex(q["weight"]) if isinstance(q["weight"], str)
+                                  else q["weight"], q["k"])
+        got = [gm.next_order_statistic(st, sc) for _ in range(q["k"])]
+        assert [t for t, _ in got] == hexs(q["times"]).tolist()
+        assert [s for _, s in got] == list(q["servers"])
+        assert st.exhausted and sorted(st.perm.tolist()) == list(range(1, q["k"] + 1))
+        with pytest.raises(gm.QueueExhaustedError):
+            gm.next_order_statistic(st, sc)
+    with pytest.raises(gm.InvalidWeightError):
+        gm.ElementQueueState(1, 0.0, 4)
+    with pytest.raises(gm.InvalidWeightError):
+        gm.ElementQueueState(1, 1e-301, 4)
