@@ -199,9 +199,20 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
   r = mod_barrett((r << 16) | ((u32)g & 0xFFFFu), m, M);
   u32 ji = zs - 1 + r;
   const u32 zi = zs - 1;
-  const u32 bj = ji & (C::NB - 1);
-  const uint4 qz = tab_bucket<C>(mytab, zi & (C::NB - 1)), qj = tab_bucket<C>(mytab, bj);
-  const u32 mz = probe_min(qz, zi), mj = probe_min(qj, ji);
+  u32 bj = ji & (C::NB - 1);
+  uint4 qz = tab_bucket<C>(mytab, zi & (C::NB - 1)), qj = tab_bucket<C>(mytab, bj);
+  u32 mz = probe_min(qz, zi), mj = probe_min(qj, ji);
+  // linear probing continues in the next bucket when the first is full:
+  // look there too before falling back to the full lookup
+  if ((mz >= 0x10000u) & (qz.w != 0u)) {
+    qz = tab_bucket<C>(mytab, (zi + 1) & (C::NB - 1));
+    mz = probe_min(qz, zi);
+  }
+  if ((mj >= 0x10000u) & (qj.w != 0u)) {
+    bj = (bj + 1) & (C::NB - 1);
+    qj = tab_bucket<C>(mytab, bj);
+    mj = probe_min(qj, ji);
+  }
   // next arrival's spacing (independent of this step's permutation work)
   const u32 zn = acc ? min(zs + 1, k) : 1u;
   const u64 x = mix64(L.ubase + (u64)zn * K_STEP);
@@ -211,7 +222,8 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
   // fast case: no draw rejection, zi resolved in its first bucket, ji found
   // in its first bucket (overwrite) or absent with a free way there (insert)
   const bool jfound = mj < 0x10000u;
-  const bool slow = acc & (((u32)(g >> 32) == 0xFFFFFFFFu) | (zs >= (u32)C::MTAB) |
+  const bool redraw = ((u32)(g >> 32) == 0xFFFFFFFFu) | (zs >= (u32)C::MTAB);  // the Barrett draw is not exact
+  const bool slow = acc & (redraw |
                            ((mz >= 0x10000u) & (qz.w != 0u)) | (!jfound & (qj.w != 0u)));
   u32 vz = mz < 0x10000u ? (mz & 0xFFFFu) + 1 : zi + 1;
   u32 vj = jfound ? (mj & 0xFFFFu) + 1 : ji + 1;
@@ -223,7 +235,9 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
   bool fresh_slot = !jfound;
   if (!L.fast) dq = __ddiv_rn(Lg, D);
   if (slow) {
-    ji = perm_draw(L.pbase, zs, k) - 1;
+    // a full first bucket alone keeps the fast draw; only a rejected draw or a
+    // step beyond the Barrett table needs the exact one
+    if (redraw) ji = perm_draw(L.pbase, zs, k) - 1;
     vz = (u32)tab_find<C>(mytab, zi) & 0xFFFFu;
     const u64 fj = tab_find<C>(mytab, ji);
     vj = (u32)fj & 0xFFFFu;
