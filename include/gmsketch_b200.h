@@ -56,6 +56,7 @@ extern "C" {
 #define GM_FLAG_EXHAUSTIVE 0x2u  /* run every queue to k (sketch_naive semantics)  */
 #define GM_FLAG_ACCUMULATE 0x4u  /* gm_sketch_elements: fold into y_io/s_io        */
 #define GM_FLAG_SPLIT 0x8u       /* gm_sketch_csr: experimental split schedule     */
+#define GM_FLAG_S32 0x10u        /* gm_sketch_csr_host: s_out is uint32 (32-bit ids) */
 
 /* Library version (major*10000 + minor*100 + patch). */
 int gm_version(void);
@@ -94,7 +95,9 @@ int gm_sketch_csr(const void *ids, int id_bits, const void *w, int w_bits,
  * locked outputs are stored by the kernel directly).  With GM_FLAG_ASYNC the
  * call only enqueues: the caller keeps the buffers untouched until `stream`
  * is synchronised.  Alternating two streams pipelines batches: one batch's
- * input copy and first CTAs overlap the previous batch's tail. */
+ * input copy and first CTAs overlap the previous batch's tail.  With
+ * GM_FLAG_S32 (32-bit ids only) s_out points to uint32 ids (an unset register
+ * reads 0xFFFFFFFF): 12 instead of 16 bytes per register cross the bus. */
 int gm_sketch_csr_host(const void *ids, int id_bits, const void *w, int w_bits,
                        const int64_t *offsets, int64_t n_vec, int32_t k,
                        uint64_t global_seed, uint64_t stream_salt,

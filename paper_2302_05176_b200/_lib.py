@@ -28,6 +28,7 @@ GM_FLAG_ASYNC = 0x1
 GM_FLAG_EXHAUSTIVE = 0x2
 GM_FLAG_ACCUMULATE = 0x4
 GM_FLAG_SPLIT = 0x8
+GM_FLAG_S32 = 0x10
 
 # every symbol include/gmsketch_b200.h declares: (name, restype, argtypes)
 _u64, _i64, _i32, _u32, _int, _vp, _dbl = (ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32,

@@ -626,36 +626,61 @@ int gm_sketch_csr_host(const void* ids, int id_bits, const void* w, int w_bits,
   Workspace* ws = nullptr;
   rc = get_ws(st, &ws);
   if (rc) return rc;
+  const bool s32 = flags & GM_FLAG_S32;
+  if (s32 && id_bits != 32) return fail(GM_ERR_INVALID_PARAMETER, "GM_FLAG_S32 needs 32-bit ids");
   const int64_t n = offsets[n_vec];
   const size_t ib = (size_t)n * (id_bits / 8), wb = (size_t)n * (w_bits / 8);
   const size_t ob = (size_t)(n_vec + 1) * 8, yb = (size_t)n_vec * k * 8;
   // results go straight to page-locked host buffers (the kernel's stores
-  // overlap its compute); pageable ones are staged on the device and copied
+  // overlap its compute); pageable ones are staged on the device and copied.
+  // GM_FLAG_S32: s is delivered as uint32 (ids are 32-bit), narrowed on the
+  // device, so the host receives 12 instead of 16 bytes per register.
   double* dy_host = (double*)pinned_device_ptr(y_out);
-  u64* ds_host = (u64*)pinned_device_ptr(s_out);
+  void* ds_host = pinned_device_ptr(s_out);
   int64_t* dem_host = (int64_t*)pinned_device_ptr(emitted_out);
-  const bool direct = dy_host && ds_host && (!emitted_out || dem_host);
+  // A synchronous call has the kernel store into page-locked outputs (the
+  // stores overlap its compute); a GM_FLAG_ASYNC call (a stream of batches)
+  // stages on the device and lets the copy engine move the registers, which
+  // overlaps the next batches' kernels instead of holding their SMs on bus
+  // writes (tools/e2e_variants.py).  GM_HOST_ZEROCOPY_OUT: 0 never, 2 always.
+  static const int zc_out = getenv("GM_HOST_ZEROCOPY_OUT") ? atoi(getenv("GM_HOST_ZEROCOPY_OUT")) : 1;
+  const bool zc = zc_out == 2 || (zc_out == 1 && !(flags & GM_FLAG_ASYNC));
+  const bool direct = zc && dy_host && ds_host && (!emitted_out || dem_host);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  const size_t need = al(ib) + al(wb) + al(ob) + (direct ? 0 : 2 * al(yb) + al((size_t)n_vec * 8));
+  const size_t sb32 = (size_t)n_vec * k * 4;
+  const size_t need = al(ib) + al(wb) + al(ob) + (direct ? 0 : al(yb) + al((size_t)n_vec * 8)) +
+                      ((!direct || s32) ? al(yb) : 0) + ((s32 && !direct) ? al(sb32) : 0);
   rc = grow((unsigned char**)&ws->stage, &ws->stage_cap, need, st);
   if (rc) return rc;
-  unsigned char* base = (unsigned char*)ws->stage;
-  void* d_ids = base;
-  void* d_w = base + al(ib);
-  int64_t* d_off = (int64_t*)(base + al(ib) + al(wb));
-  unsigned char* d_rest = (unsigned char*)d_off + al(ob);
-  double* d_y = direct ? dy_host : (double*)d_rest;
-  u64* d_s = direct ? ds_host : (u64*)(d_rest + al(yb));
-  int64_t* d_em = !emitted_out ? nullptr : direct ? dem_host : (int64_t*)(d_rest + 2 * al(yb));
+  unsigned char* p = (unsigned char*)ws->stage;
+  auto take = [&](size_t bytes) {
+    unsigned char* q = p;
+    p += al(bytes);
+    return q;
+  };
+  void* d_ids = take(ib);
+  void* d_w = take(wb);
+  int64_t* d_off = (int64_t*)take(ob);
+  double* d_y = direct ? dy_host : (double*)take(yb);
+  u64* d_s = (direct && !s32) ? (u64*)ds_host : (u64*)take(yb);
+  int64_t* d_em = !emitted_out ? nullptr : direct ? dem_host : (int64_t*)take((size_t)n_vec * 8);
+  u32* d_s32 = !s32 ? nullptr : direct ? (u32*)ds_host : (u32*)take(sb32);
   CK(cudaMemcpyAsync(d_off, offsets, ob, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_w, w, wb, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_ids, ids, ib, cudaMemcpyHostToDevice, st));
   rc = gm_sketch_csr(d_ids, id_bits, d_w, w_bits, d_off, n_vec, k, global_seed, stream_salt,
-                     flags | GM_FLAG_ASYNC, d_y, d_s, d_em, stream);
+                     (flags & ~GM_FLAG_S32) | GM_FLAG_ASYNC, d_y, d_s, d_em, stream);
   if (rc) return rc;
+  if (s32) {
+    const int64_t nr = n_vec * (int64_t)k;
+    narrow_u32_kernel<<<(unsigned)std::min<int64_t>((nr + 255) / 256, (int64_t)num_sms() * 8), 256, 0, st>>>(
+        d_s, d_s32, nr);
+    CK(cudaGetLastError());
+  }
   if (!direct) {
     CK(cudaMemcpyAsync(y_out, d_y, yb, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(s_out, d_s, yb, cudaMemcpyDeviceToHost, st));
+    if (s32) CK(cudaMemcpyAsync(s_out, d_s32, sb32, cudaMemcpyDeviceToHost, st));
+    else CK(cudaMemcpyAsync(s_out, d_s, yb, cudaMemcpyDeviceToHost, st));
     if (d_em) CK(cudaMemcpyAsync(emitted_out, d_em, (size_t)n_vec * 8, cudaMemcpyDeviceToHost, st));
   }
   // GM_FLAG_ASYNC: enqueue only (inputs and outputs stay in use until the

@@ -526,6 +526,13 @@ __global__ void __launch_bounds__(256) exact_sum_kernel(const double* __restrict
   if (card_out) card_out[sk] = __ddiv_rn((double)(k - 1), total);
 }
 
+// s narrowed to 32 bits (GM_FLAG_S32 host outputs; an unset register's
+// UINT64_MAX becomes 0xFFFFFFFF)
+__global__ void narrow_u32_kernel(const u64* __restrict__ in, u32* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (u32)in[i];
+}
+
 // ---- K0 test kernels: the keyed streams element by element ----
 __global__ void uniform_kernel(const u64* seeds, const u64* elems, const u64* steps, int64_t n,
                                double* out) {

@@ -236,14 +236,15 @@ def sketch_csr(ids, weights, offsets, k: int, scheme: SeedScheme, *, exhaustive:
 
 
 def sketch_csr_host(ids, weights, offsets, k: int, scheme: SeedScheme, *, out=None,
-                    counted: bool = False, exhaustive: bool = False, exact_y: bool = False):
+                    counted: bool = False, exhaustive: bool = False, exact_y: bool = False, s32: bool = False):
     """Host-buffer batch: ``sketch_csr`` for CPU-resident CSR arrays, through
     gm_sketch_csr_host (input copies pipelined with the sketch; results
     stored straight into page-locked outputs).  ``out=(y, s)`` supplies
     output arrays or CPU tensors (float64 / uint64-or-int64, shape
     [n_vec, k]); pin them for the zero-copy store.  Returns (y, s, emitted
     or None) as given/allocated (numpy when allocated here).  ``exact_y``:
-    see sketch_csr."""
+    see sketch_csr.  ``s32`` (32-bit ids only): s comes back as uint32
+    (GM_FLAG_S32; 12 instead of 16 bytes per register over the bus)."""
     _check_k(k)
     _device.require_cuda()
 
@@ -269,18 +270,19 @@ def sketch_csr_host(ids, weights, offsets, k: int, scheme: SeedScheme, *, out=No
     off_h, op = host(offsets, None) if isinstance(offsets, torch.Tensor) else host(offsets, np.int64)
     n_vec = int(off_h.shape[0]) - 1
     if out is None:
-        y, s = np.empty((n_vec, k), np.float64), np.empty((n_vec, k), np.uint64)
+        y, s = np.empty((n_vec, k), np.float64), np.empty((n_vec, k), np.uint32 if s32 else np.uint64)
     else:
         y, s = out
     _, yp = host(y, None)
     _, sp = host(s, None)
     em = np.zeros(max(n_vec, 1), np.int64) if counted else None
-    flags = _lib.GM_FLAG_EXHAUSTIVE if exhaustive else 0
+    flags = (_lib.GM_FLAG_EXHAUSTIVE if exhaustive else 0) | (_lib.GM_FLAG_S32 if s32 else 0)
     _device.call("gm_sketch_csr_host", ip, id_bits, wp, w_bits, op, n_vec, k, scheme.global_seed,
                  scheme.stream_salt, flags, yp, sp, em.ctypes.data if em is not None else None,
                  _device.stream_ptr())
     if exact_y:
-        exact_y_host(ids_h, w_h, off_h, k, scheme, s, y)
+        s64 = (s.numpy() if isinstance(s, torch.Tensor) else s).astype(np.uint64) if s32 else s
+        exact_y_host(ids_h, w_h, off_h, k, scheme, s64, y)
     return y, s, (em[:n_vec] if em is not None else None)
 
 

@@ -316,6 +316,12 @@ def test_host_api_matches_device_api():
         gm.sketch_csr_host(ids, w, bad, k, sc)
     y2, s2, _ = gm.sketch_csr_host(ids, w, off, k, sc)  # the error does not stick
     assert np.array_equal(s2, s)
+    # compact 32-bit s (GM_FLAG_S32), pageable and page-locked outputs
+    y3, s3, _ = gm.sketch_csr_host(ids, w, off, k, sc, s32=True)
+    assert s3.dtype == np.uint32 and np.array_equal(s3.astype(np.uint64), s) and np.array_equal(y3, y)
+    sp32 = torch.empty((n_vec, k), dtype=torch.int32).pin_memory()
+    gm.sketch_csr_host(ids, w, off, k, sc, out=(yp, sp32), s32=True)
+    assert np.array_equal(sp32.numpy().view(np.uint32).astype(np.uint64), s) and torch.equal(yp, d.y.cpu())
 
 
 def test_batches_pipelined_over_streams():
