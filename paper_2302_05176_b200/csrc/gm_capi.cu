@@ -234,15 +234,20 @@ int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n
   rc = grow(&ws->vflag, &ws->vflag_cap, (size_t)n_vec, st);
   if (rc) return rc;
   CK(cudaMemsetAsync(ws->counters, 0, sizeof(int), st));
-  if (!skip_prep) {
+  // the slots compute each vector's weight sum themselves (no prep launch)
+  // unless a vector subset re-uses sums computed earlier (skip_prep), or
+  // GM_CSR_PREP=1 asks for the separate prep kernel
+  static const bool prep_kernel = getenv("GM_CSR_PREP") && atoi(getenv("GM_CSR_PREP")) == 1;
+  const bool inkernel = !skip_prep && !prep_kernel;
+  if (!skip_prep && prep_kernel) {
     const int64_t prep_blocks = std::min<int64_t>((n_vec + 7) / 8, (int64_t)num_sms() * 16);
     csr_prep_kernel<WT><<<(unsigned)prep_blocks, 256, 0, st>>>((const WT*)w, offsets, n_vec, ws->vsum, ws->vflag,
                                                                ws->err);
     CK(cudaGetLastError());
   }
   kern<<<(unsigned)grid, C::NT, smem, st>>>((const IdT*)ids, (const WT*)w, offsets, n_vec, k, useed, pseed,
-                                            ws->vsum, ws->vflag, y, s, em, ws->counters, ws->csr_dense, ws->err,
-                                            attempt0, vec_list);
+                                            inkernel ? nullptr : ws->vsum, inkernel ? nullptr : ws->vflag, y, s, em,
+                                            ws->counters, ws->csr_dense, ws->err, attempt0, vec_list);
   CK(cudaGetLastError());
   return GM_OK;
 }

@@ -433,10 +433,16 @@ __device__ __forceinline__ void slot_open_pass(SlotInfo& sl, u32 k, int attempt,
 // warp-uniform: take the next vector of the batch into slot s (or mark it
 // empty when the batch is exhausted)
 
-template <class C>
+//
+// Wsum == nullptr: the slot computes the vector's total weight, validates
+// its weights and checks the fast-divide range itself (the prep kernel's work
+// for this vector, in the same order: the same W), so the batch needs no
+// prep launch.
+template <class C, class WT>
 __device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const int64_t* offsets,
                           int64_t n_vec, const double* Wsum, const int* vflags, int* vec_counter,
-                          unsigned long long* err, int attempt0, int lane, const int* vec_list) {
+                          unsigned long long* err, int attempt0, int lane, const int* vec_list,
+                          const WT* wts) {
   const unsigned FULL = 0xFFFFFFFFu;
   SlotInfo& sl = S.slot[s];
   for (;;) {
@@ -454,10 +460,39 @@ __device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const
     }
     if (vec_list) v = vec_list[v];  // a subset of the batch (re-runs)
     const int64_t lo = offsets[v], n = offsets[v + 1] - lo;
-    if (n <= 0) continue;  // EmptyVectorError latched by the prep kernel
+    if (n <= 0) {  // EmptyVectorError (latched here without a prep kernel)
+      if (!Wsum && lane == 0) atomicCAS(err, 0ull, ((unsigned long long)(v & 0xFFFFFFFF) << 32) | 1u);
+      continue;
+    }
     if (n > C::NMAX) {
       if (lane == 0) atomicCAS(err, 0ull, ((unsigned long long)(v & 0xFFFFFFFF) << 32) | 3u);
       continue;
+    }
+    double W = 0.0;
+    int fast = 1;
+    if (!Wsum) {
+      int bad = 0;
+      for (int64_t i0 = lo + lane; i0 < lo + n; i0 += 8 * 32) {  // 8 loads in flight per lane
+        WT wv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) wv[u] = i0 + u * 32 < lo + n ? __ldcg(&wts[i0 + u * 32]) : WT(0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (i0 + u * 32 < lo + n) {
+            const double w = (double)wv[u];
+            bad |= !(isfinite(w) && w > 0.0 && w >= 1e-300);
+            fast &= w_fast(w);
+            W += w;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) W += __shfl_xor_sync(FULL, W, o);
+      fast = __all_sync(FULL, fast);
+      if (__any_sync(FULL, bad)) {
+        if (lane == 0) atomicCAS(err, 0ull, ((unsigned long long)(v & 0xFFFFFFFF) << 32) | 2u);
+        continue;
+      }
     }
     Reg* regs = slot_regs<C>(smem, s, k);
     for (u32 j = lane; j < k; j += 32)
@@ -468,8 +503,8 @@ __device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const
       sl.v = v;
       sl.lo = lo;
       sl.n = (int)n;
-      sl.W = Wsum[v];
-      sl.fast = vflags[v] & 1;
+      sl.W = Wsum ? Wsum[v] : W;
+      sl.fast = Wsum ? (vflags[v] & 1) : fast;
       sl.emitted = 0;
       sl.seq = ++S.seq;
       slot_open_pass(sl, k, attempt0, C::kDeep);
@@ -551,7 +586,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   }
   if (tid == 0) S.seq = 0;
   __syncthreads();
-  if (warp < V) slot_load<C>(S, warp, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list);
+  if (warp < V)
+    slot_load<C, WT>(S, warp, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list,
+                     wts);
   __syncthreads();
 
   Lane L;
@@ -633,7 +670,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         GM_TRACE((unsigned long long)(v & 0xFFFFFFFF) | ((unsigned long long)att << 32) | (1ull << 40) |
                  ((unsigned long long)blockIdx.x << 48) | ((unsigned long long)s << 60));
       __syncwarp();
-      slot_load<C>(S, s, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list);
+      slot_load<C, WT>(S, s, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list,
+                       wts);
     }
 
 #ifdef GM_STATS
