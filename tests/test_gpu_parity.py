@@ -164,6 +164,11 @@ def test_config1_golden():
                       gm.SeedScheme(int(g["seed"])))
     y, s = batch_np(b)
     assert_regs(y[0], s[0], g["y"], g["s"])
+    # and bit-identical to the reference after the exact-y finalize
+    be = gm.sketch_csr(g["ids"].astype(np.uint32), g["w"], np.array([0, g["ids"].size]), int(g["k"]),
+                       gm.SeedScheme(int(g["seed"])), exact_y=True)
+    ye, se = batch_np(be)
+    assert ye[0].tobytes() == np.asarray(g["y"], np.float64).tobytes() and np.array_equal(se[0], g["s"])
     # the grid-wide kernel agrees too
     y2, s2, _ = gm.sketch_elements(g["ids"].astype(np.uint32), g["w"], int(g["k"]), gm.SeedScheme(int(g["seed"])))
     assert_regs(y2.cpu().numpy(), s2.cpu().numpy().view(np.uint64), g["y"], g["s"])
