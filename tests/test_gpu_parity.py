@@ -235,6 +235,17 @@ def test_config3_subset_vs_oracle():
     assert_regs(y, s, yo, so)
 
 
+def test_config3_full_vs_oracle():
+    """All of config 3 (1e5 vectors, 6.6e7 elements, k=512) against the oracle."""
+    import os
+    ids, w, off, k, seed = workloads.config3()
+    y, s = batch_np(gm.sketch_csr(ids, w, off, k, gm.SeedScheme(seed)))
+    rc, yo, so, _ = O.sketch_csr(ids.astype(np.uint64), w.astype(np.float64), off, k, seed, mode=0,
+                                 threads=os.cpu_count() or 8)
+    assert rc == 0
+    assert_regs(y, s, yo, so)
+
+
 def test_config4_prefix_vs_oracle():
     ids, w, k, seed = workloads.config4(n_pairs=2_000_000, n_keys=10**7)
     y, s, _ = gm.sketch_elements(ids, w, k, gm.SeedScheme(seed))
