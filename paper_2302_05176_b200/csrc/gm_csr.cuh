@@ -167,6 +167,9 @@ constexpr u32 NEED_SLOW_DRAW = 0xFFFFFFFFu;
 // finish the pending register update: a CAS that found another value (a
 // concurrent update) is retried while (t, id) is still lexicographically less
 __device__ __forceinline__ void lane_settle(Lane& L) {
+#ifndef GM_DEFER_CAS
+  return;  // register updates complete within the step (reg_min_lane)
+#endif
   if (L.pr) {
     u64 oy = L.poy, oid = L.poid;
     if (oy != L.pcy || oid != L.pcid) {
@@ -203,14 +206,15 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
   uint4 qz = tab_bucket<C>(mytab, zi & (C::NB - 1)), qj = tab_bucket<C>(mytab, bj);
   u32 mz = probe_min(qz, zi), mj = probe_min(qj, ji);
   // linear probing continues in the next bucket when the first is full:
-  // look there too before falling back to the full lookup
-  if ((mz >= 0x10000u) & (qz.w != 0u)) {
-    qz = tab_bucket<C>(mytab, (zi + 1) & (C::NB - 1));
-    mz = probe_min(qz, zi);
-  }
-  if ((mj >= 0x10000u) & (qj.w != 0u)) {
-    bj = (bj + 1) & (C::NB - 1);
+  // look there too before falling back to the full lookup (branch-free: when
+  // the first bucket settles it, the same bucket is simply read again)
+  {
+    const u32 nz = ((mz >= 0x10000u) & (qz.w != 0u)) ? 1u : 0u;
+    const u32 nj = ((mj >= 0x10000u) & (qj.w != 0u)) ? 1u : 0u;
+    bj = (bj + nj) & (C::NB - 1);
+    qz = tab_bucket<C>(mytab, (zi + nz) & (C::NB - 1));
     qj = tab_bucket<C>(mytab, bj);
+    mz = probe_min(qz, zi);
     mj = probe_min(qj, ji);
   }
   // next arrival's spacing (independent of this step's permutation work)
@@ -272,7 +276,7 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
       L.pnid = L.id;
     }
 #else
-    reg_min<true>(&L.regs[vj - 1], (u64)__double_as_longlong(L.t), L.id);
+    reg_min_lane(&L.regs[vj - 1], (u64)__double_as_longlong(L.t), L.id);
 #endif
     L.b = L.t;
     L.z = zs;
