@@ -149,41 +149,7 @@ struct Lane {
   int used;
   int slot;
   bool fast;
-  // register update in flight: a 128-bit CAS issued in one step and checked
-  // in the next, so its ~220-cycle round trip overlaps the next step's work
-  Reg* pr;           // register (nullptr: none pending)
-  u64 pcy, pcid;     // value the CAS expected
-  u64 pny, pnid;     // value it installs
-  u64 poy, poid;     // value it found
-  // software pipeline (lane_step_p): the draw of the step to accept (j - 1,
-  // or NEED_SLOW_DRAW) and the spacing quotient of the step after it, both
-  // computed one call ahead
-  u32 jz;
-  double dqn;
 };
-
-constexpr u32 NEED_SLOW_DRAW = 0xFFFFFFFFu;
-
-// finish the pending register update: a CAS that found another value (a
-// concurrent update) is retried while (t, id) is still lexicographically less
-__device__ __forceinline__ void lane_settle(Lane& L) {
-#ifndef GM_DEFER_CAS
-  return;  // register updates complete within the step (reg_min_lane)
-#endif
-  if (L.pr) {
-    u64 oy = L.poy, oid = L.poid;
-    if (oy != L.pcy || oid != L.pcid) {
-      while (lex_less(L.pny, L.pnid, oy, oid)) {
-        u64 ry, rid;
-        cas128_shared(L.pr, oy, oid, L.pny, L.pnid, ry, rid);
-        if (ry == oy && rid == oid) break;
-        oy = ry;
-        oid = rid;
-      }
-    }
-    L.pr = nullptr;
-  }
-}
 
 // One accepted queue step of the lane's element (or, when fresh, only the
 // first arrival).  Returns 0: continue, 1: element finished (first arrival
@@ -249,42 +215,19 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
     fresh_slot = sj == 0x3FFFu;
     put_slot = fresh_slot ? fr : sj;
   }
-  if (acc) {
-    if (ji == zi) {
-      vj = vz;
-    } else if (!fresh_slot || (L.used < C::CAPI && put_slot != 0x3FFFu)) {
-      tab_put<C>(mytab, put_slot, (ji << 16) | (vz - 1));
-      L.used += fresh_slot;
-    } else {
-      lane_settle(L);
-      return 2;
-    }
-#ifdef GM_DEFER_CAS
-    // the previous step's CAS has had this step's work to complete
-    lane_settle(L);
-    Reg* r = &L.regs[vj - 1];
-    const u64 ty = (u64)__double_as_longlong(L.t);
-    u64 cy, cid;
-    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
-                 : "=l"(cy), "=l"(cid) : "r"((u32)__cvta_generic_to_shared(r)) : "memory");
-    if (lex_less(ty, L.id, cy, cid)) {
-      cas128_shared(r, cy, cid, ty, L.id, L.poy, L.poid);
-      L.pr = r;
-      L.pcy = cy;
-      L.pcid = cid;
-      L.pny = ty;
-      L.pnid = L.id;
-    }
-#else
-    reg_min_lane(&L.regs[vj - 1], (u64)__double_as_longlong(L.t), L.id);
-#endif
-    L.b = L.t;
-    L.z = zs;
-  }
+  // accept step zs (branch-lean: the table write and the register update are
+  // predicated on acc; only a full table leaves the straight line)
+  const bool moved = ji != zi;
+  if (acc & moved & !(!fresh_slot || (L.used < C::CAPI && put_slot != 0x3FFFu)))
+    return 2;  // table full: hand over before step zs
+  if (!moved) vj = vz;
+  if (acc & moved) tab_put<C>(mytab, put_slot, (ji << 16) | (vz - 1));
+  L.used += (acc & moved & fresh_slot) ? 1 : 0;
+  reg_min_lane(&L.regs[vj - 1], (u64)__double_as_longlong(L.t), L.id, acc);
+  L.b = acc ? L.t : L.b;
+  L.z = acc ? zs : L.z;
   L.t = __dadd_rn(L.b, dq);
-  const int rc = (L.z >= k || L.t > L.tau) ? 1 : 0;
-  if (rc) lane_settle(L);  // the element is counted as finished after this call
-  return rc;
+  return (L.z >= k || L.t > L.tau) ? 1 : 0;
 }
 
 // One queue step zs (arrival time t) with full table lookups and the exact
@@ -307,111 +250,6 @@ __device__ __noinline__ bool lane_step_generic(Lane& L, u32 zs, double t, u32* m
   }
   reg_min<true>(&L.regs[vj - 1], (u64)__double_as_longlong(t), L.id);
   return true;
-}
-
-// ---- pipelined lane step --------------------------------------------------
-// j - 1 of step zs by the fast Barrett reduction, or NEED_SLOW_DRAW when the
-// rejection branch or a step beyond the Barrett table needs the exact draw
-template <class C>
-__device__ __forceinline__ u32 lane_draw(const Lane& L, u32 zs, const u32* mtab, u32 k) {
-  const u32 zc = min(zs, k);
-  const u64 g = mix64(L.pbase + (u64)zc * K_STEP);
-  const u32 m = k - zc + 1, M = mtab[min(zc, (u32)C::MTAB - 1)];
-  u32 r = mod_barrett((u32)(g >> 32), m, M);
-  r = mod_barrett((r << 16) | ((u32)g >> 16), m, M);
-  r = mod_barrett((r << 16) | ((u32)g & 0xFFFFu), m, M);
-  const bool bad = ((u32)(g >> 32) == 0xFFFFFFFFu) | (zc >= (u32)C::MTAB);
-  return bad ? NEED_SLOW_DRAW : zc - 1 + r;
-}
-
-// spacing quotient of step z (clamped to k) by the branch-free divide, and
-// its operands for the exact divide of elements outside its range
-__device__ __forceinline__ double lane_sp(const Lane& L, u32 z, u32 k, double& Lg, double& D) {
-  const u32 zc = min(z, k);
-  const u64 x = mix64(L.ubase + (u64)zc * K_STEP);
-  Lg = -log_pos(u_open(x));
-  D = __dmul_rn(L.w, (double)(k - zc + 1));
-  return ddiv_fast(Lg, D);
-}
-
-// Software-pipelined lane step.  A call accepts step zs = z + 1 (pending
-// arrival L.t) with the draw L.jz computed by the previous call, and starts
-// the draw of step zs + 1 and the spacing of step zs + 2 for the calls after
-// it; the register CAS issued here is checked by the next call.  So the only
-// chain a call waits on is probe -> resolve -> CAS issue; the long hash/log
-// chains of later steps run underneath.  Returns 0: continue, 1: element
-// finished, 2: table full (state before step zs kept for a warp to resume).
-template <class C>
-__device__ __forceinline__ int lane_step_p(Lane& L, bool fresh, u32* mytab, const u32* mtab, u32 k) {
-  if (fresh) {  // pending arrival of step 1, spacing of step 2, draw of step 1
-    double L1, D1, L2, D2;
-    double s1 = lane_sp(L, 1u, k, L1, D1);
-    double s2 = lane_sp(L, 2u, k, L2, D2);
-    L.jz = lane_draw<C>(L, 1u, mtab, k);
-    if (!L.fast) {
-      s1 = __ddiv_rn(L1, D1);
-      s2 = __ddiv_rn(L2, D2);
-    }
-    L.dqn = s2;
-    L.t = __dadd_rn(0.0, s1);
-    return L.t > L.tau ? 1 : 0;
-  }
-  lane_settle(L);  // the previous call's CAS: its result has had a call to arrive
-  const u32 zs = L.z + 1, zi = zs - 1;
-  const u32 jd = L.jz;
-  const bool rej = jd == NEED_SLOW_DRAW;
-  const u32 ji = rej ? zi : jd;
-  const u32 bj = ji & (C::NB - 1);
-  const uint4 qz = tab_bucket<C>(mytab, zi & (C::NB - 1)), qj = tab_bucket<C>(mytab, bj);
-  // next steps' chains (consumed by the next calls)
-  const u32 jn = lane_draw<C>(L, zs + 1, mtab, k);
-  double L2, D2;
-  double dq2 = lane_sp(L, zs + 2, k, L2, D2);
-  // resolve step zs from the pre-step table
-  const u32 mz = probe_min(qz, zi), mj = probe_min(qj, ji);
-  const bool jfound = mj < 0x10000u;
-  const bool slow = rej | ((mz >= 0x10000u) & (qz.w != 0u)) | (!jfound & (qj.w != 0u));
-  const u32 vz = mz < 0x10000u ? (mz & 0xFFFFu) + 1 : zi + 1;
-  u32 vj = jfound ? (mj & 0xFFFFu) + 1 : ji + 1;
-  const u32 k16 = ji << 16;
-  const u32 jway = jfound ? (((qj.x ^ k16) < 0x10000u) ? 0u : ((qj.y ^ k16) < 0x10000u) ? 1u
-                                                           : ((qj.z ^ k16) < 0x10000u) ? 2u : 3u)
-                          : first_empty(qj);
-  const bool moved = ji != zi;
-  if (!moved) vj = vz;
-  if (!slow && moved && !jfound && L.used >= C::CAPI) return 2;  // table full: hand over before step zs
-  if (!slow) {
-    if (moved) {
-      tab_put<C>(mytab, bj * 4 + jway, (ji << 16) | (vz - 1));
-      L.used += !jfound;
-    }
-    Reg* r = &L.regs[vj - 1];
-    const u64 ty = (u64)__double_as_longlong(L.t);
-    u64 cy, cid;
-    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
-                 : "=l"(cy), "=l"(cid) : "r"((u32)__cvta_generic_to_shared(r)) : "memory");
-    if (lex_less(ty, L.id, cy, cid)) {
-      cas128_shared(r, cy, cid, ty, L.id, L.poy, L.poid);
-      L.pr = r;
-      L.pcy = cy;
-      L.pcid = cid;
-      L.pny = ty;
-      L.pnid = L.id;
-    }
-  } else {
-    if (!lane_step_generic<C>(L, zs, L.t, mytab, k)) return 2;
-  }
-  if (!L.fast) dq2 = __ddiv_rn(L2, D2);
-  // advance: pending arrival of step zs + 1 from the spacing computed last call
-  L.b = L.t;
-  L.z = zs;
-  L.jz = jn;
-  const double dqn = L.dqn;
-  L.dqn = dq2;
-  L.t = zs < k ? __dadd_rn(L.b, dqn) : __longlong_as_double(0x7FF0000000000000ll);
-  const int rc = (L.z >= k || L.t > L.tau) ? 1 : 0;
-  if (rc) lane_settle(L);  // the element is counted as finished after this call
-  return rc;
 }
 
 // ---- vector slots ----------------------------------------------------------
@@ -603,7 +441,6 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   L.id = L.ubase = L.pbase = 0;
   L.regs = nullptr;
   L.fast = true;
-  L.pr = nullptr;
   bool live = false, fresh = false, deep = false, resume = false;
   u32 em = 0;     // arrivals computed for the current element
   u32 fin = 0;    // slots this warp must finalise (warp-uniform)
