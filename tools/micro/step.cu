@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(256, 2) kstep(unsigned long long* cyc, unsigne
   tab_clear<C>(mytab);
   __syncthreads();
   Lane L;
-  L.regs = regs; L.fast = true; L.tau = 9.43 / 1000.0; L.pr = nullptr;
+  L.regs = regs; L.fast = true; L.tau = 9.43 / 1000.0;
   u64 e = (u64)blockIdx.x * 100000 + threadIdx.x * 977;
   bool fresh = true;
   auto start = [&]() {

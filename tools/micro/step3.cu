@@ -17,7 +17,7 @@ __global__ void __launch_bounds__(256) kstep(unsigned long long* acc, int iters,
   tab_clear<C>(mytab);
   __syncthreads();
   Lane L;
-  L.regs = regs; L.fast = true; L.tau = 9.43 / 1000.0; L.pr = nullptr;
+  L.regs = regs; L.fast = true; L.tau = 9.43 / 1000.0;
   u64 e = threadIdx.x * 977;
   bool fresh = true;
   auto start = [&]() {
