@@ -254,6 +254,32 @@ def test_config4_prefix_vs_oracle():
     assert_regs(y.cpu().numpy(), s.cpu().numpy().view(np.uint64), yo, so)
 
 
+def test_elements_all_id_and_weight_widths():
+    """The elements path (filter + survivor walk) for u32/u64 ids and f32/f64
+    weights, vector-load and scalar paths (odd n, unaligned views), against
+    the oracle's stream sketch."""
+    rng = np.random.default_rng(31)
+    for n, k in [(300_001, 2048), (99_999, 512)]:
+        ids64 = rng.choice(1 << 40, n, replace=False).astype(np.uint64)
+        w64 = rng.lognormal(0.0, 1.5, n)
+        rc, yo, so, _, _ = O.sketch_stream(ids64, w64, k, 3)
+        assert rc == 0
+        for ids, w in [(ids64, w64), (ids64, w64.astype(np.float32))]:
+            wo = w.astype(np.float64)
+            rc, yo2, so2, _, _ = O.sketch_stream(ids, wo, k, 3)
+            y, s, _ = gm.sketch_elements(ids, w, k, gm.SeedScheme(3))
+            assert_regs(y.cpu().numpy(), s.cpu().numpy().view(np.uint64), yo2, so2)
+        ids32 = (np.arange(n, dtype=np.uint64) * 2654435761 % (1 << 32)).astype(np.uint32)
+        for w in (w64, w64.astype(np.float32)):
+            rc, yo3, so3, _, _ = O.sketch_stream(ids32.astype(np.uint64), w.astype(np.float64), k, 3)
+            d_ids = torch.from_numpy(ids32.view(np.int32)).cuda()
+            d_w = torch.from_numpy(w).cuda()
+            for a in (0, 1):  # offset 1: no 16-byte alignment, the scalar path
+                y, s, _ = gm.sketch_elements(d_ids[a:], d_w[a:], k, gm.SeedScheme(3))
+                rc, yo4, so4, _, _ = O.sketch_stream(ids32[a:].astype(np.uint64), w[a:].astype(np.float64), k, 3)
+                assert_regs(y.cpu().numpy(), s.cpu().numpy().view(np.uint64), yo4, so4)
+
+
 def test_config5_prefix_vs_oracle():
     n = 5_000_000
     rng = np.random.default_rng(5)
