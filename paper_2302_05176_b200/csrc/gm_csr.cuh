@@ -85,7 +85,8 @@ __host__ __device__ constexpr size_t csr3_smem_bytes(u32 k) {
          + (size_t)C::NT * C::SLOTS * 4              // lane tables
          + (size_t)C::MTAB * 4                       // Barrett table
          + 128 * 32                                  // log table copy
-         + (size_t)C::NWARP * 32 * (8 + 4);          // warp-walker scan + prov
+         + (size_t)C::NWARP * 32 * (8 + 4)           // warp-walker scan + prov
+         + (size_t)C::MTAB * 8;                      // 64-bit Barrett table
 }
 
 // ---- lane table ----------------------------------------------------------
@@ -156,17 +157,14 @@ struct Lane {
 // beyond tau or queue exhausted), 2: table full (state before the step kept
 // for a warp to resume).
 template <class C>
-__device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const u32* mtab, u32 k,
+__device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const u64* mtab64, u32 k,
                                          const double (*ltab)[4]) {
   const bool acc = !fresh;
   const u32 zs = L.z + 1;
   // permutation draw of step zs and both first-bucket probes
   const u64 g = mix64(L.pbase + (u64)zs * K_STEP);
-  const u32 m = k - zs + 1, M = mtab[min(zs, (u32)C::MTAB - 1)];
-  u32 r = mod_barrett((u32)(g >> 32), m, M);
-  r = mod_barrett((r << 16) | ((u32)g >> 16), m, M);
-  r = mod_barrett((r << 16) | ((u32)g & 0xFFFFu), m, M);
-  u32 ji = zs - 1 + r;
+  const u32 m = k - zs + 1;
+  u32 ji = zs - 1 + mod_barrett64(g, m, mtab64[min(zs, (u32)C::MTAB - 1)]);
   const u32 zi = zs - 1;
   u32 bj = ji & (C::NB - 1);
   uint4 qz = tab_bucket<C>(mytab, zi & (C::NB - 1)), qj = tab_bucket<C>(mytab, bj);
@@ -413,10 +411,16 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   double (*ltab)[4] = reinterpret_cast<double (*)[4]>(mtab + C::MTAB);  // 16-byte aligned: MTAB*4 % 16 == 0
   double* scan = reinterpret_cast<double*>(ltab + 128) + warp * 32;
   int* prov = reinterpret_cast<int*>(reinterpret_cast<double*>(ltab + 128) + NWARP * 32) + warp * 32;
+  // floor(2^64 / m) for m = k - z + 1, z < MTAB: the lane step's draw in one 64-bit Barrett reduction
+  u64* mtab64 = reinterpret_cast<u64*>(reinterpret_cast<int*>(reinterpret_cast<double*>(ltab + 128) + NWARP * 32) +
+                                       NWARP * 32);
   u32* mytab = tables + tid * 4;
   u32* dense = dense_global + ((size_t)blockIdx.x * NWARP + warp) * k;
 
-  for (u32 z = tid; z < (u32)C::MTAB; z += NT) mtab[z] = (z >= 1 && z <= k) ? barrett_magic(k - z + 1) : 0u;
+  for (u32 z = tid; z < (u32)C::MTAB; z += NT) {
+    mtab[z] = (z >= 1 && z <= k) ? barrett_magic(k - z + 1) : 0u;
+    mtab64[z] = (z >= 1 && z <= k) ? barrett_magic64(k - z + 1) : 0ull;
+  }
   for (u32 i = tid; i < 128 * 4; i += NT) ltab[i >> 2][i & 3] = gm_logtab[i >> 2][i & 3];
   tab_clear<C>(mytab);
   for (u32 i = lane; i < k; i += 32) dense[i] = 0;  // stamps restart every launch
@@ -702,7 +706,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 #pragma unroll 1
     for (int u = 0; u < C::U; ++u) {
       if (live) {
-        const int rc = lane_step<C>(L, fresh, mytab, mtab, k, ltab);
+        const int rc = lane_step<C>(L, fresh, mytab, mtab64, k, ltab);
         fresh = false;
         if (rc == 1) {
           em += L.z < k ? L.z + 1 : L.z;
