@@ -137,11 +137,14 @@ __device__ __forceinline__ u32 mix64_hi24(u64 x) {
   return (u32)((x * M2) >> 40);
 }
 
-__device__ __forceinline__ bool filter_skip_f(u64 ubase, float x) {
+__device__ __forceinline__ bool filter_skip_f(u64 key, float x) {  // key = useed + id K_ELEM + K_STEP
   float thr;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(thr) : "f"(__fmaf_rn(x, -1.4426950408889634f, 23.9996f)));
-  return (float)(mix64_hi24(ubase + K_STEP) + 1u) < thr;
+  return (float)(mix64_hi24(key) + 1u) < thr;
 }
+
+// positive, finite (fp32: any such value is >= 1e-300): one integer compare
+__device__ __forceinline__ bool weight_ok_f32(float w) { return __float_as_uint(w) - 1u < 0x7F7FFFFFu; }
 
 template <class WT>
 __device__ __forceinline__ bool weight_ok_t(WT w) {
@@ -175,16 +178,18 @@ __device__ __forceinline__ bool surv_cache_first(unsigned long long* cache, u64 
   return true;
 }
 
-// rare path: append the flagged elements (bit e of keep = element base + e * step)
+// rare path: append the flagged elements of the warp (bit e of keep / bad =
+// element base + e), one warp-aggregated atomic per element position; a
+// repeated id is listed once per CTA (surv_cache_first)
 template <class IdT>
-__device__ __noinline__ void append_flagged(u32 keep, u32 bad, int64_t base, int64_t step, int nbits, int64_t* list,
+__device__ __noinline__ void append_flagged(u32 keep, u32 bad, int64_t base, int nbits, int64_t* list,
                                             int64_t cap, unsigned long long* count, unsigned long long* err,
                                             const IdT* ids, unsigned long long* cache) {
   const int lane = threadIdx.x & 31;
   for (int e = 0; e < nbits; ++e) {
     bool kp = (keep >> e) & 1u;
-    if (kp) kp = surv_cache_first(cache, (u64)ids[base + e * step]);
-    if ((bad >> e) & 1u) raise_error(err, 2u, (u64)(base + e * step));
+    if (kp) kp = surv_cache_first(cache, (u64)ids[base + e]);
+    if ((bad >> e) & 1u) raise_error(err, 2u, (u64)(base + e));
     const unsigned m = __ballot_sync(0xFFFFFFFFu, kp);
     if (!m) continue;
     unsigned long long b = 0;
@@ -192,7 +197,7 @@ __device__ __noinline__ void append_flagged(u32 keep, u32 bad, int64_t base, int
     b = __shfl_sync(0xFFFFFFFFu, b, __ffs(m) - 1);
     if (kp) {
       const unsigned long long pos = b + __popc(m & ((1u << lane) - 1u));
-      if ((int64_t)pos < cap) list[pos] = base + e * step;
+      if ((int64_t)pos < cap) list[pos] = base + e;
     }
   }
 }
@@ -207,6 +212,7 @@ __global__ void __launch_bounds__(NT)
   __syncthreads();
   const double tk = *tau_p * (double)k;
   const float tkf = (float)tk;
+  const u64 c0 = useed + K_STEP;
   u32 skipped = 0;
   constexpr bool kVec = sizeof(WT) == 4;  // fp32 weights: float4; ids uint4 (u32) or 2 x ulonglong2 (u64)
   const int64_t tid = (int64_t)blockIdx.x * NT + threadIdx.x, nthr = (int64_t)gridDim.x * NT;
@@ -234,19 +240,18 @@ __global__ void __launch_bounds__(NT)
       }
       const float4 w0 = __ldcs(&wq[q0]), w1 = __ldcs(&wq[q1]);
       const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-      u32 keep = 0, bad = 0;
+      u32 okm = 0, skm = 0;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const bool ok = weight_ok_t(wv[e]);
-        const bool sk = filter_skip_f(useed + idv[e] * K_ELEM, tkf * wv[e]);
-        bad |= (u32)!ok << e;
-        keep |= (u32)(ok && !sk) << e;
-        skipped += ok && sk;
+        okm |= (u32)weight_ok_f32(wv[e]) << e;
+        skm |= (u32)filter_skip_f(c0 + idv[e] * K_ELEM, tkf * wv[e]) << e;
       }
+      const u32 keep = okm & ~skm, bad = ~okm & 0xFFu;
+      skipped += __popc(okm & skm);
+      // bit e: quad q0 (e < 4) or q1 (e >= 4), element e & 3
       if (__any_sync(0xFFFFFFFFu, (keep | bad) != 0u)) {
-        // bit e: quad q0 (e < 4) or q1 (e >= 4), element e & 3
-        append_flagged(keep & 15u, bad & 15u, 4 * q0, 1, 4, list, cap, count, err, ids, cache);
-        append_flagged(keep >> 4, bad >> 4, 4 * q1, 1, 4, list, cap, count, err, ids, cache);
+        append_flagged(keep & 15u, bad & 15u, 4 * q0, 4, list, cap, count, err, ids, cache);
+        append_flagged(keep >> 4, bad >> 4, 4 * q1, 4, list, cap, count, err, ids, cache);
       }
     }
     first = rounds * 2 * nthr * 4;
@@ -257,13 +262,13 @@ __global__ void __launch_bounds__(NT)
     if (i0 < n) {
       const WT w = __ldcs(&wts[i0]);
       const bool ok = weight_ok_t(w);
-      const bool sk = ok && filter_skip_f(useed + (u64)__ldcs(&ids[i0]) * K_ELEM, filter_x(w, tkf, tk));
+      const bool sk = ok && filter_skip_f(c0 + (u64)__ldcs(&ids[i0]) * K_ELEM, filter_x(w, tkf, tk));
       bad = !ok;
       keep = ok && !sk;
       skipped += sk;
     }
     if (__any_sync(0xFFFFFFFFu, (keep | bad) != 0u))
-      append_flagged(keep, bad, i0, 1, 1, list, cap, count, err, ids, cache);
+      append_flagged(keep, bad, i0, 1, list, cap, count, err, ids, cache);
   }
   if (emitted_total) {
     unsigned long long e = skipped;
