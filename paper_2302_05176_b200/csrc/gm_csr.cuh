@@ -697,6 +697,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     }
     GM_STAT(1, lane == 0);  // lane-step iterations
     GM_STAT(2, live);       // live lanes summed over them
+    GM_STAT(5, deep);       // lanes waiting for a warp walk
+    GM_STAT(6, !live && !deep && qcnt == 0 && qnext == 0);  // idle: the warp's queue is empty
+    GM_STAT(7, !live && !deep && (qcnt != 0 || qnext != 0));  // idle although entries are queued
 
 #ifdef GM_STATS
     { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 13; }

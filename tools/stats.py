@@ -36,12 +36,14 @@ L.gm_stats_read(buf)
 gm.sketch_csr(d_ids, d_w, d_off, k, gm.SeedScheme(seed))
 torch.cuda.synchronize()
 L.gm_stats_read(buf)
-names = ["idle iters", "step iters", "live lane-steps", "warp walks", "warp-walk arrivals", "accepted lane-steps",
-         "valid lane-steps", "loop iterations"]
+names = ["idle iters", "step iters", "live lane-steps", "warp walks", "warp-walk arrivals", "deep lanes at steps",
+         "idle lanes, queue empty", "idle lanes, entries queued"]
 for i, nme in enumerate(names):
     print(f"{nme:22s} {buf[i]:>14,d}")
 sec = {8: "finalise", 9: "warp walks", 10: "refill", 11: "start", 12: "exit/idle", 13: "lane steps", 14: "completions"}  # section after each marker
 tot = sum(buf[i] for i in sec) or 1
 for i, nme in sec.items():
     print(f"  cycles {nme:12s} {100 * buf[i] / tot:5.1f}%")
-print(f"lanes per round live: {buf[2] / max(buf[1], 1):.2f} groups of 8; accepted/valid {buf[5] / max(buf[6], 1):.3f}")
+it = max(buf[1], 1)
+print(f"per step iteration (of 32 lanes): live {buf[2] / it:.2f}, deep {buf[5] / it:.2f}, idle/queue empty {buf[6] / it:.2f}, "
+      f"idle/entries queued {buf[7] / it:.2f}")
