@@ -1,3 +1,4 @@
+"""Debug: one config-2 CSR batch on the device against the oracle, per-register diff report (GPU box)."""
 import ctypes, os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

@@ -1,3 +1,4 @@
+"""Debug: naive (exhaustive) sketches of the golden vector cases on the device against the fixtures (GPU box)."""
 import os, sys, json
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

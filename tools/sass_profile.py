@@ -18,8 +18,12 @@ def lineinfo(kname):
     so = os.path.join(ROOT, "paper_2302_05176_b200", "libgmsketch_b200.so")
     with tempfile.TemporaryDirectory() as d:
         subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=d, capture_output=True)
-        cub = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
-        txt = subprocess.run(["nvdisasm", "-g", os.path.join(d, cub)], capture_output=True, text=True).stdout
+        txt = ""
+        for cub in sorted(f for f in os.listdir(d) if f.endswith(".cubin")):  # the cubin holding the kernel
+            t = subprocess.run(["nvdisasm", "-g", os.path.join(d, cub)], capture_output=True, text=True).stdout
+            if any(ln.startswith(".text.") and kname in ln for ln in t.splitlines()):
+                txt = t
+                break
     lines = txt.splitlines()
     start = next(i for i, ln in enumerate(lines) if ln.startswith(".text.") and kname in ln)
     cur = None
