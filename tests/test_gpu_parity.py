@@ -461,6 +461,10 @@ def test_errors_map_to_reference_classes():
         gm.sketch_elements(np.array([1, 2], np.uint32), np.array([1.0, 0.0]), 8, sc)
     with pytest.raises(gm.MismatchedSketchError):
         gm.merge([])
+    with pytest.raises(gm.InvalidParameterError):  # 32-bit s for 64-bit ids
+        gm.sketch_csr_host(np.array([1 << 40], np.uint64), np.array([1.0]), np.array([0, 1]), 8, sc, s32=True)
+    with pytest.raises(gm.InvalidParameterError):
+        gm.estimate_cardinality_batch(gm.sketch_csr(np.array([1], np.uint32), np.array([1.0]), np.array([0, 1]), 1, sc))
     # the library recovers after a data error
     sk = gm.sketch_fast(gm.WeightedVector({1: 1.0}), gm.GenerationParams(k=4, scheme=sc))
     assert sk.s == (1, 1, 1, 1)
