@@ -175,11 +175,12 @@ int num_sms() {
   return sms;
 }
 
-using CsrDefault = CsrCfg<256, 16, 2, 2, 75>;
-// alternates for tuning sweeps (GM_CSR_CFG=1..3 selects one for u32 ids + f32 weights)
-using CsrAlt1 = CsrCfg<256, 16, 2, 2, 75>;
-using CsrAlt2 = CsrCfg<256, 16, 2, 2, 85>;
-using CsrAlt3 = CsrCfg<256, 16, 2, 2, 95>;
+using CsrDefault = CsrCfg<256, 16, 2, 2, 75, 4>;
+// alternates for tuning sweeps (GM_CSR_CFG=1..3 selects one for u32 ids + f32 weights;
+// 1 = without the drain hand-over)
+using CsrAlt1 = CsrCfg<256, 16, 2, 2, 75, 0>;
+using CsrAlt2 = CsrCfg<256, 16, 2, 2, 85, 4>;
+using CsrAlt3 = CsrCfg<256, 16, 2, 2, 95, 4>;
 
 int csr_cfg_choice() {
   static int c = -1;

@@ -37,8 +37,9 @@
 
 namespace gmk {
 
-template <int NT_, int NB_, int V_ = 2, int MINB_ = 1, int DEEP_PCT_ = 62>
+template <int NT_, int NB_, int V_ = 2, int MINB_ = 1, int DEEP_PCT_ = 62, int DRAIN_LIVE_ = 0>
 struct CsrCfg {
+  static constexpr int DRAIN_LIVE = DRAIN_LIVE_;  // queue empty and <= this many live lanes: warp-walk them
   static constexpr int NT = NT_;               // threads per CTA
   static constexpr int NWARP = NT_ / 32;
   static constexpr int MINB = MINB_;           // __launch_bounds__ min blocks
@@ -704,6 +705,18 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 #ifdef GM_STATS
     { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 13; }
 #endif
+    // ---- drain: the warp's queue is empty and few lanes still walk -- hand
+    // their elements to the warp walker (all 32 lanes on each, next iteration)
+    // instead of stepping with a mostly idle warp
+    if (C::DRAIN_LIVE > 0 && qcnt == 0 && qnext == 0 && __popc(__ballot_sync(FULL, live)) <= C::DRAIN_LIVE) {
+      if (live) {
+        em += L.z;
+        live = false;
+        deep = true;
+        resume = true;
+      }
+      continue;
+    }
     // ---- (5) C::U lane steps (a lane whose element ends idles for the rest)
     bool done = false;
 #pragma unroll 1
