@@ -59,6 +59,7 @@ from .sketch import (
     compute_ri,
     sketch_csr,
     sketch_csr_host,
+    sketch_csr_host_many,
     exact_y_host,
     sketch_elements,
     sketch_fast,

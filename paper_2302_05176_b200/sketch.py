@@ -312,6 +312,55 @@ def exact_y_host(ids, weights, offsets, k: int, scheme: SeedScheme, s, y, thread
     return y
 
 
+def sketch_csr_host_many(batches, k: int, scheme: SeedScheme, *, streams: int = 6, s32: bool = False):
+    """A stream of host-buffer CSR batches (the serving loop): yields (y, s)
+    per batch, in order, with batches issued over ``streams`` CUDA streams so
+    one batch's copies and first CTAs overlap the previous batches' kernels
+    (GM_FLAG_ASYNC).  ``batches`` yields (ids, weights,
+    offsets) numpy arrays (u32/u64 ids, f32/f64 weights); each result is a
+    pair of page-locked CPU tensors valid until ``streams`` more batches have
+    been issued (copy them to keep them longer)."""
+    _check_k(k)
+    dev = _device.require_cuda()
+    pool = [torch.cuda.Stream(device=dev) for _ in range(max(1, streams))]
+    inflight = []  # (stream index, y, s, keep-alive inputs)
+    outs = {}
+
+    def issue(i, b):
+        ids, w, off = b
+        a_ids, id_bits = _device.id_array(ids)
+        a_w, w_bits = _device.weight_array(w)
+        a_off = np.ascontiguousarray(np.asarray(off, dtype=np.int64))
+        n_vec = a_off.size - 1
+        t_ids = torch.from_numpy(a_ids.view(np.int32 if id_bits == 32 else np.int64)).pin_memory()
+        t_w = torch.from_numpy(a_w).pin_memory()
+        t_off = torch.from_numpy(a_off).pin_memory()
+        j = i % len(pool)
+        key = (j, n_vec)
+        if key not in outs or outs[key][0].shape[0] != n_vec:
+            outs[key] = (torch.empty((n_vec, k), dtype=torch.float64).pin_memory(),
+                         torch.empty((n_vec, k), dtype=torch.int32 if s32 else torch.int64).pin_memory())
+        y, s = outs[key]
+        flags = _lib.GM_FLAG_ASYNC | (_lib.GM_FLAG_S32 if s32 else 0)
+        _device.call("gm_sketch_csr_host", t_ids.data_ptr(), id_bits, t_w.data_ptr(), w_bits, t_off.data_ptr(), n_vec,
+                     k, scheme.global_seed, scheme.stream_salt, flags, y.data_ptr(), s.data_ptr(), None,
+                     pool[j].cuda_stream)
+        inflight.append((j, y, s, (t_ids, t_w, t_off)))
+
+    def retire():
+        j, y, s, _ = inflight.pop(0)
+        pool[j].synchronize()
+        _device.call("gm_stream_status", pool[j].cuda_stream)
+        return y, s
+
+    for i, b in enumerate(batches):
+        if len(inflight) == len(pool):
+            yield retire()
+        issue(i, b)
+    while inflight:
+        yield retire()
+
+
 def _as_id_np(ids) -> np.ndarray:
     a, bits = _device.id_array(ids)
     return a.view(np.int32 if bits == 32 else np.int64)

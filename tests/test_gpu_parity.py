@@ -400,6 +400,23 @@ def test_batches_pipelined_over_streams():
         assert torch.equal(hs[i], ref.s.cpu()) and torch.equal(hy[i], ref.y.cpu())
 
 
+def test_host_batches_stream_api():
+    """sketch_csr_host_many: a stream of host batches over several CUDA
+    streams returns every batch's registers, in order, equal to sketch_csr."""
+    ids, w, off, k, seed = workloads.config2(n_vectors=200)
+    sc = gm.SeedScheme(seed)
+    ref = gm.sketch_csr(ids, w, off, k, sc)
+    parts = [(0, 50), (50, 120), (120, 200)] * 3
+    batches = [(ids[off[a]:off[b]], w[off[a]:off[b]], off[a:b + 1] - off[a]) for a, b in parts]
+    got = [(y.clone(), s.clone()) for y, s in gm.sketch_csr_host_many(iter(batches), k, sc, streams=4)]
+    assert len(got) == len(parts)
+    for (a, b), (y, s) in zip(parts, got):
+        assert torch.equal(s, ref.s[a:b].cpu()) and torch.equal(y, ref.y[a:b].cpu())
+    got32 = [s.clone() for _, s in gm.sketch_csr_host_many(iter(batches[:3]), k, sc, streams=2, s32=True)]
+    for (a, b), s in zip(parts[:3], got32):
+        assert torch.equal(s.to(torch.int64) & 0xFFFFFFFF, ref.s[a:b].cpu())
+
+
 # ---------------------------------------------------------------- edge cases
 def test_single_element_owns_every_register():
     for k in (1, 3, 64, 1024, 4096):
