@@ -317,27 +317,48 @@ def sketch_csr_host_many(batches, k: int, scheme: SeedScheme, *, streams: int = 
     per batch, in order, with batches issued over ``streams`` CUDA streams so
     one batch's copies and first CTAs overlap the previous batches' kernels
     (GM_FLAG_ASYNC).  ``batches`` yields (ids, weights,
-    offsets) numpy arrays (u32/u64 ids, f32/f64 weights); each result is a
-    pair of page-locked CPU tensors valid until ``streams`` more batches have
-    been issued (copy them to keep them longer)."""
+    offsets) numpy arrays or CPU tensors (u32/u64 ids, f32/f64 weights;
+    page-locked tensors are used in place, anything else is copied into a
+    reused page-locked staging buffer per stream); each result is a pair of
+    page-locked CPU tensors that stay valid while ``streams`` more results
+    are taken from the generator (copy them to keep them longer)."""
     _check_k(k)
     dev = _device.require_cuda()
     pool = [torch.cuda.Stream(device=dev) for _ in range(max(1, streams))]
     inflight = []  # (stream index, y, s, keep-alive inputs)
     outs = {}
 
+    staging = {}  # per stream: page-locked input buffers, reused (grown when needed)
+
+    def pinned(j, name, a):
+        t = torch.from_numpy(a) if isinstance(a, np.ndarray) else a
+        if t.is_pinned():
+            return t
+        buf = staging.get((j, name))
+        if buf is None or buf.numel() < t.numel() or buf.dtype != t.dtype:
+            buf = torch.empty(max(t.numel(), 1), dtype=t.dtype).pin_memory()
+            staging[(j, name)] = buf
+        view = buf[: t.numel()]
+        view.copy_(t.reshape(-1))
+        return view
+
     def issue(i, b):
         ids, w, off = b
-        a_ids, id_bits = _device.id_array(ids)
-        a_w, w_bits = _device.weight_array(w)
-        a_off = np.ascontiguousarray(np.asarray(off, dtype=np.int64))
-        n_vec = a_off.size - 1
-        t_ids = torch.from_numpy(a_ids.view(np.int32 if id_bits == 32 else np.int64)).pin_memory()
-        t_w = torch.from_numpy(a_w).pin_memory()
-        t_off = torch.from_numpy(a_off).pin_memory()
         j = i % len(pool)
-        key = (j, n_vec)
-        if key not in outs or outs[key][0].shape[0] != n_vec:
+        if isinstance(ids, torch.Tensor):
+            id_bits, t_ids = _device.id_bits_of(ids), ids
+        else:
+            a_ids, id_bits = _device.id_array(ids)
+            t_ids = a_ids.view(np.int32 if id_bits == 32 else np.int64)
+        if isinstance(w, torch.Tensor):
+            w_bits, t_w = _device.w_bits_of(w), w
+        else:
+            t_w, w_bits = _device.weight_array(w)
+        t_off = off if isinstance(off, torch.Tensor) else np.ascontiguousarray(np.asarray(off, dtype=np.int64))
+        t_ids, t_w, t_off = pinned(j, "ids", t_ids), pinned(j, "w", t_w), pinned(j, "off", t_off)
+        n_vec = t_off.numel() - 1
+        key = (i % (2 * len(pool)), n_vec)  # two output sets per stream: a result outlives `streams` more yields
+        if key not in outs:
             outs[key] = (torch.empty((n_vec, k), dtype=torch.float64).pin_memory(),
                          torch.empty((n_vec, k), dtype=torch.int32 if s32 else torch.int64).pin_memory())
         y, s = outs[key]

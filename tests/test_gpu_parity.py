@@ -412,6 +412,13 @@ def test_host_batches_stream_api():
     assert len(got) == len(parts)
     for (a, b), (y, s) in zip(parts, got):
         assert torch.equal(s, ref.s[a:b].cpu()) and torch.equal(y, ref.y[a:b].cpu())
+    # a result stays valid while `streams` more are taken (no clone)
+    held = []
+    for n, (y, s) in enumerate(gm.sketch_csr_host_many(iter(batches), k, sc, streams=3)):
+        held.append((parts[n], y, s))
+        if len(held) > 3:
+            (a, b), y0, s0 = held.pop(0)
+            assert torch.equal(s0, ref.s[a:b].cpu()) and torch.equal(y0, ref.y[a:b].cpu())
     got32 = [s.clone() for _, s in gm.sketch_csr_host_many(iter(batches[:3]), k, sc, streams=2, s32=True)]
     for (a, b), s in zip(parts[:3], got32):
         assert torch.equal(s.to(torch.int64) & 0xFFFFFFFF, ref.s[a:b].cpu())
