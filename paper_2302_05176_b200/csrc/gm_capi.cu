@@ -4,7 +4,10 @@
 // launch configuration, the pass loop of gm_sketch_elements, error mapping.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstdarg>
+#include <limits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -46,8 +49,8 @@ struct Workspace {
   int* counters = nullptr;                 // [0] vector ticket, [1] unset registers
   unsigned long long* err = nullptr;       // latched data error
   unsigned long long* ull = nullptr;       // [0] heavy count, [1] emitted total
-  double* dbl = nullptr;                   // [0] tau, [1] weight sample sum
-  unsigned long long* host = nullptr;      // pinned readback (4 words)
+  double* dbl = nullptr;                   // [0] tau, [1] sampled weight, [2] sampled distinct weight, [3] tau_hi
+  unsigned long long* host = nullptr;      // pinned readback / upload (8 words)
   Reg* regs = nullptr;
   size_t regs_cap = 0;
   u64* heavy = nullptr;
@@ -84,8 +87,12 @@ struct Workspace {
   size_t vsum_cap = 0;
   int* vflag = nullptr;                    // per-vector flags (CSR prep)
   size_t vflag_cap = 0;
-  int64_t* surv = nullptr;                 // K2 filter survivors
+  Surv* surv = nullptr;                    // K2 filter survivors (id, weight)
   size_t surv_cap = 0;
+  unsigned long long* sample_set = nullptr;  // K2 weight-sample id set
+  size_t sample_set_cap = 0;
+  double* sample_part = nullptr;           // K2 weight-sample per-block partial sums
+  size_t sample_part_cap = 0;
   void* stage = nullptr;                   // device staging for *_host calls
   size_t stage_cap = 0;
   u64* pt_keys = nullptr;                  // gm_check_pairs id table
@@ -115,7 +122,7 @@ int get_ws(cudaStream_t st, Workspace** out) {
   CK(cudaMalloc(&w->err, sizeof(unsigned long long)));
   CK(cudaMalloc(&w->ull, 4 * sizeof(unsigned long long)));
   CK(cudaMalloc(&w->dbl, 4 * sizeof(double)));
-  CK(cudaMallocHost(&w->host, 4 * sizeof(unsigned long long)));
+  CK(cudaMallocHost(&w->host, 8 * sizeof(unsigned long long)));
   CK(cudaMemset(w->counters, 0, 4 * sizeof(int)));
   CK(cudaMemset(w->err, 0, sizeof(unsigned long long)));
   CK(cudaDeviceSynchronize());
@@ -341,9 +348,19 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
     init_regs_kernel<<<rgrid, 256, 0, st>>>(ws->regs, k, ws->counters + 1);
   CK(cudaGetLastError());
   if (n > 0) {
-    const int64_t sample = 1 << 20;
-    const int64_t step = n > sample ? n / sample : 1;
-    weight_sample_kernel<WT><<<256, 256, 0, st>>>((const WT*)w, n, step, ws->dbl + 1);
+    // blocked weight sample (~2^18 items in 1024 coalesced runs of 256)
+    const int sgrid = 1024;
+    int64_t sampled = 0;
+    for (int64_t b = 0; b < sgrid; ++b) {
+      const int64_t lo = b * n / sgrid;
+      sampled += std::min<int64_t>(lo + SAMPLE_RUN, (b + 1) * n / sgrid) - lo;
+    }
+    const u32 tcap = 1u << 20;  // >= 4 x the sample
+    if ((rc = grow(&ws->sample_set, &ws->sample_set_cap, (size_t)tcap, st))) return rc;
+    CK(cudaMemsetAsync(ws->sample_set, 0xFF, (size_t)tcap * sizeof(unsigned long long), st));
+    if ((rc = grow(&ws->sample_part, &ws->sample_part_cap, (size_t)(2 * sgrid), st))) return rc;
+    weight_sample_kernel<IdT, WT><<<sgrid, 256, 0, st>>>((const IdT*)ids, (const WT*)w, n, ws->sample_set, tcap,
+                                                         ws->sample_part);
     CK(cudaGetLastError());
     const int64_t heavy_need = std::min<int64_t>(n, (int64_t)1 << 22);
     rc = grow(&ws->heavy, &ws->heavy_cap, (size_t)heavy_need, st);
@@ -355,28 +372,57 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&light_per_sm, elem_light_kernel<IdT, WT>, NT, 0));
     int64_t lgrid = (int64_t)light_per_sm * num_sms();
     lgrid = std::min<int64_t>(lgrid, (n + NT - 1) / NT);
-    // filter pass (HBM-streaming first-arrival test, survivors compacted)
-    // for finite thresholds; the fused light kernel when tau is +inf, when
-    // the survivor list overflows, or with GM_ELEM_FUSED=1
+    // filter pass (HBM-streaming first-arrival test against the list bound
+    // tau_hi, survivors compacted into a list)
+    // for finite thresholds; a failed pass whose next tau is still <= tau_hi
+    // re-walks the list instead of streaming the input again.  The fused light
+    // kernel serves tau = +inf, a survivor-list overflow and GM_ELEM_FUSED=1.
     static const bool fused_only = getenv("GM_ELEM_FUSED") && atoi(getenv("GM_ELEM_FUSED")) == 1;
     const int64_t surv_cap = std::min<int64_t>(n, (int64_t)1 << 26);
     if ((rc = grow(&ws->surv, &ws->surv_cap, (size_t)surv_cap, st))) return rc;
     const int64_t fgrid = std::min<int64_t>((n / 4 + 2 * NT - 1) / (2 * NT) + 1, (int64_t)num_sms() * 8);
+    const double lk = std::log((double)k);
+    double tau_h = 0.0, tau_hi_h = 0.0, R = 2.0;
+    bool list_ok = false;  // the survivor list holds every element with first arrival <= tau_hi_h
     for (int attempt = 0;; ++attempt) {
       const int att = (flags & GM_FLAG_EXHAUSTIVE) ? 5 : attempt;
-      tau_kernel<<<1, 1, 0, st>>>(ws->dbl, ws->dbl + 1, k, att, ws->counters + 1);
+      bool rebuild = true;
+      if (att >= 5) {  // +inf: full queues (sketch_naive)
+        tau_h = tau_hi_h = std::numeric_limits<double>::infinity();
+      } else if (attempt > 0) {  // from the unset fraction f: P(unset) = exp(-W tau)
+        const int unset = (int)(ws->host[0] & 0xFFFFFFFFull);
+        const double f = (double)unset / (double)k;
+        const double W_est = f < 1.0 ? -std::log(f) / tau_h : 0.0;
+        const double next = W_est > 0.0 ? std::max((lk + 3.0 + 2.0 * attempt) / W_est, 2.0 * tau_h)
+                                        : tau_h * (double)k;
+        tau_h = next;
+        if (list_ok && next <= tau_hi_h) rebuild = false;
+        else tau_hi_h = R * next;
+      }
+      if (att >= 5 || attempt > 0) {
+        double* up = reinterpret_cast<double*>(ws->host + 6);
+        up[0] = tau_h;
+        up[1] = tau_hi_h;
+        CK(cudaMemcpyAsync(ws->dbl, up, sizeof(double), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(ws->dbl + 3, up + 1, sizeof(double), cudaMemcpyHostToDevice, st));
+      } else {
+        tau_kernel<<<1, 256, 0, st>>>(ws->dbl, ws->sample_part, sgrid, k, (double)n / (double)std::max<int64_t>(sampled, 1));
+      }
       CK(cudaMemsetAsync(ws->ull, 0, sizeof(unsigned long long), st));
       bool use_filter = !fused_only && att < 4;
       for (int round = 0; round < 2; ++round) {
         if (use_filter) {
-          CK(cudaMemsetAsync(ws->ull + 2, 0, sizeof(unsigned long long), st));
-          elem_filter_kernel<IdT, WT><<<(unsigned)fgrid, NT, 0, st>>>(
-              (const IdT*)ids, (const WT*)w, n, k, useed, ws->dbl, ws->surv, surv_cap, ws->ull + 2,
-              emitted_out ? ws->ull + 1 : nullptr, ws->err);
-          CK(cudaGetLastError());
-          elem_survivor_kernel<IdT, WT><<<(unsigned)(num_sms() * 4), NT, 0, st>>>(
-              (const IdT*)ids, (const WT*)w, ws->surv, ws->ull + 2, surv_cap, k, useed, pseed, ws->dbl, ws->regs,
-              ws->counters + 1, ws->heavy, (int64_t)ws->heavy_cap, ws->ull, emitted_out ? ws->ull + 1 : nullptr);
+          if (rebuild) {
+            CK(cudaMemsetAsync(ws->ull + 2, 0, sizeof(unsigned long long), st));
+            elem_filter_kernel<IdT, WT><<<(unsigned)fgrid, NT, 0, st>>>(
+                (const IdT*)ids, (const WT*)w, n, k, useed, ws->dbl + 3, ws->surv, surv_cap,
+                ws->ull + 2, emitted_out ? ws->ull + 1 : nullptr, ws->err);
+            CK(cudaGetLastError());
+          }
+          elem_survivor_kernel<<<(unsigned)(num_sms() * 4), NT, 0, st>>>(
+              ws->surv, ws->ull + 2, surv_cap, k, useed, pseed, ws->dbl,
+              ws->regs, ws->counters + 1, ws->heavy, (int64_t)ws->heavy_cap, ws->ull,
+              emitted_out ? ws->ull + 1 : nullptr);
         } else {
           elem_light_kernel<IdT, WT><<<(unsigned)lgrid, NT, 0, st>>>(
               (const IdT*)ids, (const WT*)w, n, k, useed, pseed, ws->dbl, ws->regs, ws->counters + 1,
@@ -384,16 +430,26 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
         }
         CK(cudaGetLastError());
         elem_heavy_kernel<IdT, WT><<<(unsigned)heavy_blocks, NT, 0, st>>>(
-            (const IdT*)ids, (const WT*)w, k, useed, pseed, ws->dbl, ws->regs, ws->counters + 1,
+            (const IdT*)ids, (const WT*)w, use_filter ? ws->surv : nullptr, k, useed, pseed, ws->dbl, ws->regs,
+            ws->counters + 1,
             ws->heavy, ws->ull, (int64_t)ws->heavy_cap, ws->dense,
             emitted_out ? ws->ull + 1 : nullptr);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(ws->host, ws->counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(ws->host + 1, ws->ull, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(ws->host + 3, ws->ull + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        if (attempt == 0 && att < 5) CK(cudaMemcpyAsync(ws->host + 4, ws->dbl, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        if (attempt == 0 && att < 5) {
+          const double* d = reinterpret_cast<const double*>(ws->host + 4);
+          tau_h = d[0];
+          tau_hi_h = d[3];
+          R = tau_h > 0.0 ? std::max(2.0, tau_hi_h / tau_h) : 2.0;
+        }
+        if (use_filter) list_ok = true;
         if (use_filter && (int64_t)ws->host[3] > surv_cap) {  // list overflow: redo the pass fused (idempotent)
           use_filter = false;
+          list_ok = false;
           CK(cudaMemsetAsync(ws->ull, 0, sizeof(unsigned long long), st));
           continue;
         }

@@ -119,28 +119,35 @@ __global__ void __launch_bounds__(NT)
 }
 
 // ---- K2 filter pass: stream the element arrays once at HBM speed --------
-// Every element's first arrival is tested with an fp32 bound (no fp64, no
-// log): u1 = (h >> 11) 2^-53 + 2^-54 < ((h >> 40) + 1) 2^-24, and the element
-// is skipped when ((h >> 40) + 1) < 2^24 (1 - 2^-12) exp(-tau k w), the right
-// side taken as ex2.approx(fma(x, -log2 e, 23.9996)) (24 + log2(1 - 2.8e-4)) with
-// x = tau k w in fp32.  Error budget: the fp32 roundings of tau k and x move
-// the exponent by <= 104 * 2^-23 (beyond 104 the threshold is 0 and nothing
-// is skipped), the fma by <= 150 * 2^-24, ex2.approx by ~2^-22 -- together
-// < 2^-15, well inside the 2.8e-4 margin, so an element is skipped only if its
-// exact fp64 first arrival exceeds tau.  Only bits 40..63 of the hash are
-// needed, and mix64's final xor-shift leaves them unchanged.  The few
-// survivors (~k (ln k + c) per pass) are compacted into a list for the walk
-// kernel; u32 ids with fp32 weights are read as uint4/float4.
-__device__ __forceinline__ u32 mix64_hi24(u64 x) {
+// Every element's first arrival is tested against the LIST bound tau_hi
+// (>= the pass threshold tau) with an fp32 test that needs no
+// log, no divide, no MUFU and no fp64: with h23 the top 23 bits of the
+// uniform hash, u1 = (h >> 11) 2^-53 + 2^-54 <= (h23 + 1) 2^-23, and
+// e^-x >= 1 - x, so the element is skipped when
+//   (h23 + 1) < A (1 - x),  A = 2^23 (1 - 2^-12),  x = tau_hi k w,
+// evaluated as  float(2^23 + h23) < fma(x, -A, A + 2^23 - 1)  (the left side
+// is the bit pattern 0x4B000000 | h23, exact).  Error budget: x carries
+// <= 2e-7 relative error (two fp32 roundings), the fma rounds by <= 0.5 (the
+// result is below 2^24, ulp 1); both stay inside the 2^-12 margin (an
+// effective 2^-13 in the log domain for every x), so an element
+// is skipped only if its exact fp64 first arrival exceeds tau_hi.  For x
+// beyond ~1 the right side drops below 2^23 and the element is kept (the
+// exact walk decides).  mix64's final xor-shift leaves bits 41..63 unchanged,
+// so the last shift is not computed.  Survivors (~k (ln k + c) tau_hi / tau
+// per pass) are compacted into a list, so the walk kernel can re-walk the
+// list for any tau <= tau_hi (a failed pass) without streaming the element
+// arrays again.
+__device__ __forceinline__ u32 mix64_hi23(u64 x) {
   x = (x ^ (x >> 30)) * M1;
   x = x ^ (x >> 27);
-  return (u32)((x * M2) >> 40);
+  return (u32)((x * M2) >> 41);
 }
 
+constexpr float FILTER_A = 8388608.0f * (1.0f - 0x1p-12f);           // 2^23 (1 - 2^-12)
+constexpr float FILTER_B = 8388608.0f * (1.0f - 0x1p-12f) + 8388607.0f;  // A + 2^23 - 1 (exact)
+
 __device__ __forceinline__ bool filter_skip_f(u64 key, float x) {  // key = useed + id K_ELEM + K_STEP
-  float thr;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(thr) : "f"(__fmaf_rn(x, -1.4426950408889634f, 23.9996f)));
-  return (float)(mix64_hi24(key) + 1u) < thr;
+  return __uint_as_float(0x4B000000u | mix64_hi23(key)) < __fmaf_rn(x, -FILTER_A, FILTER_B);
 }
 
 // positive, finite (fp32: any such value is >= 1e-300): one integer compare
@@ -163,12 +170,17 @@ __device__ __forceinline__ float filter_x(WT w, float tkf, double tk) {
 // Survivor ids already listed by this CTA in this pass: a repeated id (a
 // stream duplicate: same weight, hence the same arrivals) is a register
 // no-op, so it is listed once per CTA instead of once per occurrence (Zipf
-// streams repeat their hot keys millions of times).  Open addressing, 8
-// probes, then it is simply listed again.
+// streams repeat their hot keys millions of times).  The streaming loop
+// drops a kept element whose id sits in its home slot with one shared load
+// (a hot key already listed: no call, no atomic); first sightings insert
+// (open addressing, 8 probes, then the id is simply listed again).
 constexpr int SURV_CACHE = 1024;
 
-__device__ __forceinline__ bool surv_cache_first(unsigned long long* cache, u64 id) {
-  u32 h = (u32)(mix64(id ^ 0x2545F4914F6CDD1Dull) >> 32) & (SURV_CACHE - 1);
+__device__ __forceinline__ u32 surv_slot(u64 id) {
+  return (((u32)(id >> 32) * 0x9E3779B1u) ^ ((u32)id * 0x85EBCA6Bu)) >> 22;  // 10 bits
+}
+
+__device__ __forceinline__ bool surv_cache_first(unsigned long long* cache, u32 h, u64 id) {
   for (int p = 0; p < 8; ++p) {
     const unsigned long long prev = atomicCAS(&cache[h], ~0ull, (unsigned long long)id);
     if (prev == ~0ull) return true;   // inserted: first occurrence here
@@ -178,39 +190,84 @@ __device__ __forceinline__ bool surv_cache_first(unsigned long long* cache, u64 
   return true;
 }
 
-// rare path: append the flagged elements of the warp (bit e of keep / bad =
-// element base + e), one warp-aggregated atomic per element position; a
-// repeated id is listed once per CTA (surv_cache_first)
-template <class IdT>
-__device__ __noinline__ void append_flagged(u32 keep, u32 bad, int64_t base, int nbits, int64_t* list,
-                                            int64_t cap, unsigned long long* count, unsigned long long* err,
-                                            const IdT* ids, unsigned long long* cache) {
+// A listed survivor: its id and weight (widened to fp64 exactly), so the
+// walk kernels read 16 contiguous bytes per entry instead of gathering from
+// the element arrays.
+struct __align__(16) Surv {
+  u64 id;
+  double w;
+};
+
+// Kept elements are staged per warp in shared memory (WBUF entries) and
+// listed in bulk: the streaming loop only stores each kept (id, weight)
+// (one warp-wide prefix sum per iteration that keeps anything), and
+// flush_kept handles 32 staged entries per step lane-parallel -- insert the
+// id into the CTA's id set (first sightings only), one atomic per step for
+// the list position.  Per-element work at the moment an element is kept would
+// run at 1/32 of the warp's width (lanes hold kept elements one at a time).
+constexpr int WBUF = 256;
+
+__device__ __noinline__ void flush_kept(const Surv* wbuf, u32 wcount, Surv* list, int64_t cap,
+                                        unsigned long long* count, unsigned long long* cache) {
   const int lane = threadIdx.x & 31;
-  for (int e = 0; e < nbits; ++e) {
-    bool kp = (keep >> e) & 1u;
-    if (kp) kp = surv_cache_first(cache, (u64)ids[base + e]);
-    if ((bad >> e) & 1u) raise_error(err, 2u, (u64)(base + e));
+  __syncwarp();
+  for (u32 j0 = 0; j0 < wcount; j0 += 32) {
+    const u32 j = j0 + lane;
+    bool kp = j < wcount;
+    Surv v{0, 0.0};
+    if (kp) {
+      v = wbuf[j];
+      kp = surv_cache_first(cache, surv_slot(v.id), v.id);
+    }
     const unsigned m = __ballot_sync(0xFFFFFFFFu, kp);
     if (!m) continue;
-    unsigned long long b = 0;
-    if (lane == __ffs(m) - 1) b = atomicAdd(count, (unsigned long long)__popc(m));
-    b = __shfl_sync(0xFFFFFFFFu, b, __ffs(m) - 1);
-    if (kp) {
-      const unsigned long long pos = b + __popc(m & ((1u << lane) - 1u));
-      if ((int64_t)pos < cap) list[pos] = base + e;
-    }
+    unsigned long long base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(count, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xFFFFFFFFu, base, __ffs(m) - 1);
+    const unsigned long long pos = base + __popc(m & ((1u << lane) - 1u));
+    if (kp && (int64_t)pos < cap) list[pos] = v;
   }
+  __syncwarp();
+}
+
+// stage the kept elements of one iteration (bit e of keep: idv[e], wv[e]);
+// returns the warp's new staged count
+template <int NE, class WV>
+__device__ __forceinline__ u32 stage_kept(u32 keep, const u64 (&idv)[NE], const WV (&wv)[NE], Surv* wbuf,
+                                          u32 wcount, Surv* list, int64_t cap, unsigned long long* count,
+                                          unsigned long long* cache) {
+  const int lane = threadIdx.x & 31;
+  const u32 c = __popc(keep);
+  u32 incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const u32 total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  if (wcount + total > (u32)WBUF) {
+    flush_kept(wbuf, wcount, list, cap, count, cache);
+    wcount = 0;
+  }
+  u32 pos = wcount + incl - c;
+#pragma unroll
+  for (int e = 0; e < NE; ++e)
+    if ((keep >> e) & 1u) wbuf[pos++] = Surv{idv[e], (double)wv[e]};
+  return wcount + total;
 }
 
 template <class IdT, class WT>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, 4)
     elem_filter_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, int64_t n, u32 k, u64 useed,
-                       const double* __restrict__ tau_p, int64_t* __restrict__ list, int64_t cap,
-                       unsigned long long* count, unsigned long long* emitted_total, unsigned long long* err) {
+                       const double* __restrict__ tau_hi_p, Surv* __restrict__ list, int64_t cap, unsigned long long* count, unsigned long long* emitted_total,
+                       unsigned long long* err) {
   __shared__ unsigned long long cache[SURV_CACHE];
+  __shared__ Surv wbuf_all[NWARP * WBUF];
   for (int i = threadIdx.x; i < SURV_CACHE; i += NT) cache[i] = ~0ull;
   __syncthreads();
-  const double tk = *tau_p * (double)k;
+  Surv* wbuf = wbuf_all + (threadIdx.x >> 5) * WBUF;
+  u32 wcount = 0;
+  const double tk = *tau_hi_p * (double)k;
   const float tkf = (float)tk;
   const u64 c0 = useed + K_STEP;
   u32 skipped = 0;
@@ -246,30 +303,40 @@ __global__ void __launch_bounds__(NT)
         okm |= (u32)weight_ok_f32(wv[e]) << e;
         skm |= (u32)filter_skip_f(c0 + idv[e] * K_ELEM, tkf * wv[e]) << e;
       }
-      const u32 keep = okm & ~skm, bad = ~okm & 0xFFu;
+      u32 keep = okm & ~skm;
+      const u32 bad = ~okm & 0xFFu;
       skipped += __popc(okm & skm);
-      // bit e: quad q0 (e < 4) or q1 (e >= 4), element e & 3
-      if (__any_sync(0xFFFFFFFFu, (keep | bad) != 0u)) {
-        append_flagged(keep & 15u, bad & 15u, 4 * q0, 4, list, cap, count, err, ids, cache);
-        append_flagged(keep >> 4, bad >> 4, 4 * q1, 4, list, cap, count, err, ids, cache);
+      if (keep) {  // drop ids this CTA has listed already (hot stream keys)
+        const volatile unsigned long long* vc = cache;
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (((keep >> e) & 1u) && vc[surv_slot(idv[e])] == (unsigned long long)idv[e]) keep &= ~(1u << e);
       }
+      // bit e: quad q0 (e < 4) or q1 (e >= 4), element e & 3
+      if (__any_sync(0xFFFFFFFFu, keep != 0u))
+        wcount = stage_kept(keep, idv, wv, wbuf, wcount, list, cap, count, cache);
+      if (bad) raise_error(err, 2u, (u64)((__ffs(bad) - 1 < 4 ? 4 * q0 : 4 * q1 - 4) + __ffs(bad) - 1));
     }
     first = rounds * 2 * nthr * 4;
   }
   // scalar path: everything (no vector loads) or what the full rounds left
   for (int64_t i0 = first + tid; i0 - tid < n; i0 += nthr) {
     u32 keep = 0, bad = 0;
+    u64 idv[1] = {0};
+    WT wv[1] = {WT(1)};
     if (i0 < n) {
-      const WT w = __ldcs(&wts[i0]);
-      const bool ok = weight_ok_t(w);
-      const bool sk = ok && filter_skip_f(c0 + (u64)__ldcs(&ids[i0]) * K_ELEM, filter_x(w, tkf, tk));
+      wv[0] = __ldcs(&wts[i0]);
+      idv[0] = (u64)__ldcs(&ids[i0]);
+      const bool ok = weight_ok_t(wv[0]);
+      const bool sk = ok && filter_skip_f(c0 + idv[0] * K_ELEM, filter_x(wv[0], tkf, tk));
       bad = !ok;
       keep = ok && !sk;
       skipped += sk;
     }
-    if (__any_sync(0xFFFFFFFFu, (keep | bad) != 0u))
-      append_flagged(keep, bad, i0, 1, list, cap, count, err, ids, cache);
+    if (__any_sync(0xFFFFFFFFu, keep != 0u)) wcount = stage_kept(keep, idv, wv, wbuf, wcount, list, cap, count, cache);
+    if (bad) raise_error(err, 2u, (u64)i0);
   }
+  if (wcount) flush_kept(wbuf, wcount, list, cap, count, cache);
   if (emitted_total) {
     unsigned long long e = skipped;
 #pragma unroll
@@ -279,13 +346,15 @@ __global__ void __launch_bounds__(NT)
 }
 
 // survivors of the filter: walk light elements lane-parallel (as the fused
-// light kernel does); heavy or table-full ones go to the heavy list
-template <class IdT, class WT>
+// light kernel does); heavy or table-full ones go to the heavy list (as
+// list positions).  A listed element whose first arrival lies beyond this
+// pass's tau (the list was built for tau_hi >= tau) emits that one arrival
+// and stops.
 __global__ void __launch_bounds__(NT)
-    elem_survivor_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, const int64_t* __restrict__ list,
-                         const unsigned long long* count, int64_t cap, u32 k, u64 useed, u64 pseed,
-                         const double* __restrict__ tau_p, Reg* regs, int* unset_ctr, u64* __restrict__ heavy_list,
-                         int64_t heavy_cap, unsigned long long* heavy_count, unsigned long long* emitted_total) {
+    elem_survivor_kernel(const Surv* __restrict__ list, const unsigned long long* count, int64_t cap, u32 k,
+                         u64 useed, u64 pseed, const double* __restrict__ tau_p, Reg* regs, int* unset_ctr,
+                         u64* __restrict__ heavy_list, int64_t heavy_cap, unsigned long long* heavy_count,
+                         unsigned long long* emitted_total) {
   __shared__ u32 maps[16 * NT];
   const double tau = *tau_p;
   const double light_w = 8.0 / ((double)k * tau);
@@ -293,14 +362,12 @@ __global__ void __launch_bounds__(NT)
   u32 emitted = 0;
   u32* mymap = maps + threadIdx.x;
   for (int64_t j = (int64_t)blockIdx.x * NT + threadIdx.x; j < m; j += (int64_t)gridDim.x * NT) {
-    const int64_t i = list[j];
-    const double w = load_w(wts, i);
-    const u64 id = load_id(ids, i);
+    const Surv v = list[j];
     bool ok = false;
-    if (w < light_w) ok = walk_light<false>(id, w, tau, k, useed, pseed, mymap, NT, 16, regs, unset_ctr, emitted);
+    if (v.w < light_w) ok = walk_light<false>(v.id, v.w, tau, k, useed, pseed, mymap, NT, 16, regs, unset_ctr, emitted);
     if (!ok) {
       const unsigned long long h = atomicAdd(heavy_count, 1ull);
-      if ((int64_t)h < heavy_cap) heavy_list[h] = (u64)i;
+      if ((int64_t)h < heavy_cap) heavy_list[h] = (u64)j;
     }
   }
   if (emitted_total) {
@@ -311,11 +378,13 @@ __global__ void __launch_bounds__(NT)
   }
 }
 
-// one warp per heavy element; dense arrays in global scratch, one per warp
+// one warp per heavy element; dense arrays in global scratch, one per warp.
+// Heavy-list entries index the survivor list when `surv` is given (after the
+// filter), the element arrays otherwise (after the fused light kernel).
 template <class IdT, class WT>
 __global__ void __launch_bounds__(NT)
-    elem_heavy_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, u32 k, u64 useed,
-                      u64 pseed, const double* __restrict__ tau_p, Reg* regs, int* unset_ctr,
+    elem_heavy_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, const Surv* __restrict__ surv,
+                      u32 k, u64 useed, u64 pseed, const double* __restrict__ tau_p, Reg* regs, int* unset_ctr,
                       const u64* __restrict__ heavy_list, const unsigned long long* heavy_count,
                       int64_t heavy_cap, u32* __restrict__ dense_global,
                       unsigned long long* emitted_total) {
@@ -335,7 +404,10 @@ __global__ void __launch_bounds__(NT)
       stamp = 1;
     }
     u32 em = 0;
-    walk_warp<false>(load_id(ids, i), load_w(wts, i), tau, k, useed, pseed, dense, stamp,
+    // heavy-list entries are survivor-list positions (surv != null) or element indices
+    const u64 id = surv ? surv[i].id : load_id(ids, i);
+    const double w = surv ? surv[i].w : load_w(wts, i);
+    walk_warp<false>(id, w, tau, k, useed, pseed, dense, stamp,
                      scan_all + warp * 32, prov_all + warp * 32, regs, unset_ctr, em);
     if (lane == 0) emitted += em;
   }
@@ -371,48 +443,114 @@ __global__ void store_regs_kernel(const Reg* regs, u32 k, double* y, u64* s) {
   }
 }
 
-// tau from the total weight, or from the unset fraction f of the previous
-// pass (P(register unset) = exp(-W tau) => W ~ -ln f / tau).
-__global__ void tau_kernel(double* tau, const double* wsum, u32 k, int attempt, const int* unset_ctr) {
-  if (threadIdx.x || blockIdx.x) return;
+// First pass threshold and list bound from the sampled weights (per-block
+// partials: all sampled weight, and the sampled weight of ids seen for the
+// first time in the sample; both scaled by n / sampled items).  tau = (ln k + 3) / W
+// with W the duplicate-corrected estimate; the filter lists every element
+// whose first arrival is <= tau_hi = R tau, R = 2 x the sample's duplication
+// ratio (in [2, 256]): a stream whose sample under-counts its duplicates (a
+// Zipf stream: the sample sees few repeats of the rare keys) gets a first
+// tau that is too small, and the next pass re-walks the list with a larger
+// tau instead of streaming the input again (gm_capi.cu run_elements).
+// (one block of 256 threads; the partials are summed in a fixed order)
+__global__ void __launch_bounds__(256) tau_kernel(double* tau, const double* part, int nblocks, u32 k, double scale) {
+  __shared__ double red[2][256];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nblocks; i += 256) {
+    a += part[2 * i];
+    b += part[2 * i + 1];
+  }
+  red[0][threadIdx.x] = a;
+  red[1][threadIdx.x] = b;
+  __syncthreads();
+  for (int h = 128; h; h >>= 1) {
+    if ((int)threadIdx.x < h) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + h];
+      red[1][threadIdx.x] += red[1][threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x) return;
   const double lk = log((double)k);
-  if (attempt == 0) {
-    *tau = (lk + 3.0) / *wsum;
-    return;
-  }
-  const double prev = *tau;
-  const int unset = *unset_ctr;
-  const double f = (double)unset / (double)k;
-  double W_est = f < 1.0 ? -log(f) / prev : 0.0;
-  double next;
-  if (attempt >= 5)
-    next = __longlong_as_double(0x7FF0000000000000ll);
-  else if (W_est > 0.0)
-    next = fmax((lk + 3.0 + 2.0 * attempt) / W_est, 2.0 * prev);
-  else
-    next = prev * (double)k;
-  *tau = next;
+  double all = red[0][0], dist = red[1][0];
+  all *= scale;
+  dist *= scale;
+  tau[1] = all;
+  tau[2] = dist;
+  const double W = dist > 0.0 ? dist : all;
+  const double ratio = (dist > 0.0 && all > dist) ? all / dist : 1.0;
+  const double R = fmin(fmax(2.0 * ratio, 2.0), 256.0);
+  tau[3] = R * (lk + 3.0) / W;
+  // a stream with visible duplication walks the list at tau_hi right away:
+  // its first tau would come from an over-estimated W, and a failed walk costs
+  // a host round trip and a second walk (the list walk is ~1 arrival per
+  // listed element either way)
+  tau[0] = ratio > 1.5 ? tau[3] : (lk + 3.0) / W;
 }
 
-// weight sum (for the first tau) over a strided sample, scaled to n
-template <class WT>
-__global__ void weight_sample_kernel(const WT* __restrict__ wts, int64_t n, int64_t step,
-                                     double* out) {
-  double s = 0.0;
-  int64_t cnt = 0;
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * step; i < n;
-       i += (int64_t)gridDim.x * blockDim.x * step) {
+// Blocked sample of the stream: block b of the grid reads the contiguous
+// items [b n / G, b n / G + L) (L = min(SAMPLE_RUN, n / G), coalesced), and
+// sums their weights and the weights of ids not seen before in the sample
+// (a global hash set of `tcap` slots, power of two, all ~0 on entry; a plain
+// load settles repeats of hot keys without an atomic; id ~0 is never
+// inserted and counts as new).  Per-block partials out[2b], out[2b+1];
+// tau_kernel sums them and scales by n / sampled.
+constexpr int SAMPLE_RUN = 256;
+
+template <class IdT, class WT>
+__global__ void weight_sample_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, int64_t n,
+                                     unsigned long long* table, u32 tcap, double* out) {
+  const int64_t lo = (int64_t)blockIdx.x * n / gridDim.x;
+  const int64_t hi = min(lo + (int64_t)SAMPLE_RUN, ((int64_t)blockIdx.x + 1) * n / gridDim.x);
+  double s = 0.0, sd = 0.0;
+  const volatile unsigned long long* vt = table;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const double w = (double)wts[i];
-    if (isfinite(w) && w > 0.0) s += w;
-    ++cnt;
+    if (!(isfinite(w) && w > 0.0)) continue;
+    s += w;
+    const u64 id = (u64)ids[i];
+    bool fresh = true;
+    if (id != ~0ull) {
+      u32 h = (u32)(mix64(id) >> 32) & (tcap - 1);
+      for (;;) {
+        if (vt[h] == (unsigned long long)id) {  // repeat of a hot key: no atomic
+          fresh = false;
+          break;
+        }
+        const unsigned long long prev = atomicCAS(&table[h], ~0ull, (unsigned long long)id);
+        if (prev == ~0ull) break;
+        if (prev == (unsigned long long)id) {
+          fresh = false;
+          break;
+        }
+        h = (h + 1) & (tcap - 1);
+      }
+    }
+    if (fresh) sd += w;
   }
-  s *= (double)step;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    sd += __shfl_xor_sync(0xFFFFFFFFu, sd, o);
+  }
+  __shared__ double red[2][32];
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[0][warp] = s;
+    red[1][warp] = sd;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // per-block partials, summed in block order by tau_kernel (deterministic)
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      a += red[0][i];
+      b += red[1][i];
+    }
+    out[2 * blockIdx.x] = a;
+    out[2 * blockIdx.x + 1] = b;
+  }
 }
 
-// ---- K4 merge ----
 __global__ void merge_kernel(const double* __restrict__ y_in, const u64* __restrict__ s_in,
                              int64_t n_sk, u32 k, double* __restrict__ y_out,
                              u64* __restrict__ s_out) {
