@@ -13,7 +13,11 @@ reported as config.batch_latency_ms.  e2e runs the same stream of batches
 through gm_sketch_csr_host with page-locked host buffers (every step copies
 its 8 MB of input in and its 16 MB of registers out).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2|3|4|5]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2|3|4|5] [--n N]
+
+--config 4 / 5: one sketch of the Zipf stream (1e8 pairs, k=4096) / the huge
+vector (1e9 elements, k=8192) per step; N > 1 shards the elements and merges
+the per-rank sketches (strong scaling).
 
 N > 1 (torchrun): vectors are sharded across ranks by element count, no
 collective on the data path (scaling "weak": every rank sketches its own
@@ -51,15 +55,23 @@ def parse():
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", type=int, default=2, choices=[2, 3])
+    p.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5])
+    p.add_argument("--n", type=float, default=0, help="configs 4/5: override the element count (default: BASELINE size)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--streams", type=int, default=6, help="CUDA streams the batches rotate over")
     return p.parse_args()
 
 
-def load_workload(cfg: int):
+def load_workload(cfg: int, n: int = 0):
     from paper_2302_05176_b200 import workloads
 
+    if cfg == 4:
+        ids, w, k, seed = workloads.config4(n_pairs=n or 10**8)
+        return ids, w, None, k, seed, (f"config4: {ids.size:.3g} (u64 id, f32 weight) Zipf(1.1) stream pairs over 1e7 keys, "
+                                       "key weights U(0.1,10), k=4096")
+    if cfg == 5:
+        ids, w, k, seed = workloads.config5(n=n or 10**9)
+        return ids, w, None, k, seed, f"config5: one vector of {ids.size:.3g} elements (u32 ids 0..n-1), f32 LogNormal(0,2), k=8192"
     if cfg == 2:
         ids, w, off, k, seed = workloads.config2()
         desc = "config2: 1000 vectors x 1000 ids over 1e6, fp32 Exp(1), k=1024, pairs (2i,2i+1)"
@@ -148,8 +160,11 @@ def run_reference(args, rank, world):
     """--impl reference: the reference algorithm on the host CPU, rank 0 only."""
     if rank != 0:
         return
-    ids, w, off, k, seed, desc = load_workload(args.config)
+    ids, w, off, k, seed, desc = load_workload(args.config, int(args.n))
     threads = os.cpu_count() or 1
+    if off is None:
+        run_reference_elements(args, world, ids, w, k, seed, desc, threads)
+        return
     n_vec = off.size - 1
     # bounded sample per step: a prefix of the batch sized for ~10 s of CPU work in total
     probe_dt, probe_n = cpu_oracle_time(ids, w, off, k, seed, min(n_vec, 64), threads)
@@ -177,6 +192,190 @@ def run_reference(args, rank, world):
                                    "oracle/gm_oracle.c sketch_fast (bit-exact C port of sketch.py:218-311)"},
         "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_stream_time(ids, w, k, seed, n_sample, threads):
+    """Time the C port of the reference's sketch_stream (oracle/) over the
+    first n_sample items, split into `threads` contiguous chunks sketched in
+    parallel (ctypes releases the GIL) and merged (the partition law,
+    estimate.py:103-125); returns seconds."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+
+    ids64 = ids[:n_sample].astype(np.uint64)
+    w64 = w[:n_sample].astype(np.float64)
+    bounds = np.linspace(0, n_sample, threads + 1).astype(np.int64)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        parts = list(ex.map(lambda r: O.sketch_stream(ids64[bounds[r]:bounds[r + 1]], w64[bounds[r]:bounds[r + 1]], k, seed),
+                            [r for r in range(threads) if bounds[r + 1] > bounds[r]]))
+    ys = np.stack([p[1] for p in parts])
+    ss = np.stack([p[2] for p in parts])
+    O.merge(ys, ss)
+    return time.perf_counter() - t0
+
+
+def run_reference_elements(args, world, ids, w, k, seed, desc, threads):
+    """--impl reference for configs 4/5: the reference's sketch_stream (C port)
+    over a bounded prefix of the stream on all host threads."""
+    n = ids.size
+    probe = min(n, 200_000)
+    per_item = cpu_stream_time(ids, w, k, seed, probe, threads) / probe
+    budget = max(1.0, 8.0 / max(1, args.steps + args.warmup))
+    n_sample = int(min(n, max(probe, budget / max(per_item, 1e-12))))
+    for _ in range(args.warmup):
+        cpu_stream_time(ids, w, k, seed, n_sample, threads)
+    total = sum(cpu_stream_time(ids, w, k, seed, n_sample, threads) for _ in range(args.steps))
+    value = n_sample * args.steps / total
+    line = {
+        "impl": "reference", "metric": "positive elements sketched/sec at k=%d" % k, "value": value,
+        "unit": "elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, workloads.py)",
+        "config": {"workload": desc, "sample_items_per_step": n_sample, "parallelism": f"host threads x{threads}"},
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": threads, "kind": "port",
+                         "sample": f"first {n_sample} of {n} items per step, oracle/gm_oracle.c sketch_stream "
+                                   f"(bit-exact C port of stream.py:58-153) in {threads} chunks + merge"},
+        "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours_elements(args, rank, world, local_rank):
+    """Configs 4-5: one sketch of a huge element set.  N > 1: contiguous
+    element shards, a sketch per rank, then one exchange (all-gather of k x
+    16 B over NCCL + the device merge, shard.merge_across_ranks) -- strong
+    scaling, the whole job's elements per step are fixed."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2302_05176_b200 as gm
+    from paper_2302_05176_b200 import _device, _lib, shard
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    L = _lib.load()
+    ids, w, _, k, seed, desc = load_workload(args.config, int(args.n))
+    scheme = gm.SeedScheme(seed)
+    n_all = ids.size
+    lo, hi = shard.element_range(n_all, world, rank)
+    id_bits = ids.dtype.itemsize * 8
+    h_ids_np, h_w_np = ids[lo:hi], w[lo:hi]
+    n = hi - lo
+    d_ids = torch.from_numpy(h_ids_np.view(np.int64 if id_bits == 64 else np.int32)).to(dev)
+    d_w = torch.from_numpy(h_w_np).to(dev)
+    y = torch.empty(k, dtype=torch.float64, device=dev)
+    s = torch.empty(k, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    def step():
+        rc = L.gm_sketch_elements(d_ids.data_ptr(), id_bits, d_w.data_ptr(), 32, n, k, scheme.global_seed,
+                                  scheme.stream_salt, 0, y.data_ptr(), s.data_ptr(), 0, sp)
+        if rc:
+            raise RuntimeError(_lib.last_error())
+        if world > 1:
+            return shard.merge_across_ranks(y, s)
+        return y, s
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clocks:
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.steps):
+            yo, so = step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+    total_ms = a0.elapsed_time(a1)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    step_ms = total_ms / args.steps
+    value = n_all / (step_ms / 1e3)
+
+    # end to end: host buffers through gm_sketch_elements_host (every step copies
+    # the shard in and the k registers out), merged across ranks on the host side
+    h_ids = torch.from_numpy(h_ids_np.view(np.int64 if id_bits == 64 else np.int32)).pin_memory()
+    h_w = torch.from_numpy(h_w_np).pin_memory()
+    h_y = torch.empty(k, dtype=torch.float64).pin_memory()
+    h_s = torch.empty(k, dtype=torch.int64).pin_memory()
+
+    def e2e_step():
+        rc = L.gm_sketch_elements_host(h_ids.data_ptr(), id_bits, h_w.data_ptr(), 32, n, k, scheme.global_seed,
+                                       scheme.stream_salt, 0, h_y.data_ptr(), h_s.data_ptr(), 0, sp)
+        if rc:
+            raise RuntimeError(_lib.last_error())
+        if world > 1:
+            return shard.merge_across_ranks(h_y.to(dev), h_s.to(dev))
+        return h_y, h_s
+
+    e2e_steps = max(1, min(args.steps, 5))
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ye, se = e2e_step()
+    torch.cuda.synchronize()
+    e2e_ms = 1e3 * (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    assert torch.equal(ye.cpu(), yo.cpu()) and torch.equal(se.cpu(), so.cpu()), "host-buffer path differs from the device path"
+
+    if rank != 0:
+        return
+    hbm_peak, hbm_kind = peaks()
+    in_bytes = n * (ids.itemsize + w.itemsize)
+    achieved = in_bytes / (step_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"traffic_config{args.config}.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        threads = os.cpu_count() or 1
+        probe = min(n_all, 200_000)
+        per_item = cpu_stream_time(ids, w, k, seed, probe, threads) / probe
+        n_sample = int(min(n_all, max(probe, 10.0 / max(per_item, 1e-12))))
+        dt = cpu_stream_time(ids, w, k, seed, n_sample, threads)
+        cpu = {"value": n_sample / dt, "unit": "elements/s", "cores": threads, "kind": "port",
+               "sample": f"first {n_sample} of {n_all} items, oracle/gm_oracle.c sketch_stream in {threads} chunks + merge"}
+    line = {
+        "metric": "positive elements sketched/sec at k=%d" % k,
+        "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, workloads.py)",
+        "config": {"workload": desc, "elements_per_step": n_all, "k": k,
+                   "parallelism": f"element shards x{world} + NCCL all-gather/device merge" if world > 1 else "single GPU",
+                   "l2": f"inputs ({(ids.nbytes + w.nbytes) >> 20} MiB) larger than the 126 MB L2"},
+        "e2e": {"value": n_all / (e2e_ms / 1e3), "unit": "elements/s", "h2d_bytes_per_step": in_bytes,
+                "d2h_bytes_per_step": 16 * k, "ms_per_step": e2e_ms,
+                "api": "gm_sketch_elements_host (pinned host buffers), wall clock"},
+        "gpu_launches": 7 * args.steps + (args.steps if world > 1 else 0),
+        "gpu_launches_note": "per sketch: init, weight sample, tau, filter, survivor walk, heavy walk, store "
+                             "(+ merge for N > 1) when the first walk completes every register",
+        "roofline": {"bound": "hbm", "unit": "GB/s", "achieved": achieved, "peak": hbm_peak, "frac": achieved / hbm_peak,
+                     "traffic": traffic, "peak_kind": hbm_kind,
+                     "achieved_note": "input bytes (ids + weights) per sketch / whole sketch step (all its kernels)"},
+        "clocks": clocks.summary(),
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
 
 
@@ -413,7 +612,10 @@ def main():
 
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    run_ours(args, rank, world, local_rank)
+    if args.config in (4, 5):
+        run_ours_elements(args, rank, world, local_rank)
+    else:
+        run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
 
