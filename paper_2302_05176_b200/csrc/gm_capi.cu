@@ -378,6 +378,9 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
     // re-walks the list instead of streaming the input again.  The fused light
     // kernel serves tau = +inf, a survivor-list overflow and GM_ELEM_FUSED=1.
     static const bool fused_only = getenv("GM_ELEM_FUSED") && atoi(getenv("GM_ELEM_FUSED")) == 1;
+    // schedule knobs for tests: scale the first tau, fix the list ratio R
+    static const double tau_scale = getenv("GM_ELEM_TAU_SCALE") ? atof(getenv("GM_ELEM_TAU_SCALE")) : 1.0;
+    static const double r_fixed = getenv("GM_ELEM_R") ? atof(getenv("GM_ELEM_R")) : 0.0;
     const int64_t surv_cap = std::min<int64_t>(n, (int64_t)1 << 26);
     if ((rc = grow(&ws->surv, &ws->surv_cap, (size_t)surv_cap, st))) return rc;
     const int64_t fgrid = std::min<int64_t>((n / 4 + 2 * NT - 1) / (2 * NT) + 1, (int64_t)num_sms() * 8);
@@ -406,7 +409,8 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
         CK(cudaMemcpyAsync(ws->dbl, up, sizeof(double), cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(ws->dbl + 3, up + 1, sizeof(double), cudaMemcpyHostToDevice, st));
       } else {
-        tau_kernel<<<1, 256, 0, st>>>(ws->dbl, ws->sample_part, sgrid, k, (double)n / (double)std::max<int64_t>(sampled, 1));
+        tau_kernel<<<1, 256, 0, st>>>(ws->dbl, ws->sample_part, sgrid, k, (double)n / (double)std::max<int64_t>(sampled, 1),
+                                      tau_scale, r_fixed);
       }
       CK(cudaMemsetAsync(ws->ull, 0, sizeof(unsigned long long), st));
       bool use_filter = !fused_only && att < 4;

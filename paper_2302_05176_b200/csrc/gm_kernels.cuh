@@ -453,7 +453,8 @@ __global__ void store_regs_kernel(const Reg* regs, u32 k, double* y, u64* s) {
 // tau that is too small, and the next pass re-walks the list with a larger
 // tau instead of streaming the input again (gm_capi.cu run_elements).
 // (one block of 256 threads; the partials are summed in a fixed order)
-__global__ void __launch_bounds__(256) tau_kernel(double* tau, const double* part, int nblocks, u32 k, double scale) {
+__global__ void __launch_bounds__(256) tau_kernel(double* tau, const double* part, int nblocks, u32 k, double scale,
+                                                  double tau_scale, double r_fixed) {
   __shared__ double red[2][256];
   double a = 0.0, b = 0.0;
   for (int i = threadIdx.x; i < nblocks; i += 256) {
@@ -479,13 +480,14 @@ __global__ void __launch_bounds__(256) tau_kernel(double* tau, const double* par
   tau[2] = dist;
   const double W = dist > 0.0 ? dist : all;
   const double ratio = (dist > 0.0 && all > dist) ? all / dist : 1.0;
-  const double R = fmin(fmax(2.0 * ratio, 2.0), 256.0);
-  tau[3] = R * (lk + 3.0) / W;
+  const double R = r_fixed > 0.0 ? r_fixed : fmin(fmax(2.0 * ratio, 2.0), 256.0);
+  const double t0 = tau_scale * (lk + 3.0) / W;
+  tau[3] = R * t0;
   // a stream with visible duplication walks the list at tau_hi right away:
   // its first tau would come from an over-estimated W, and a failed walk costs
   // a host round trip and a second walk (the list walk is ~1 arrival per
   // listed element either way)
-  tau[0] = ratio > 1.5 ? tau[3] : (lk + 3.0) / W;
+  tau[0] = (ratio > 1.5 && r_fixed <= 0.0) ? tau[3] : t0;
 }
 
 // Blocked sample of the stream: block b of the grid reads the contiguous

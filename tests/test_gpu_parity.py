@@ -618,3 +618,56 @@ def test_device_log_matches_glibc():
     assert d.max() <= 1
     assert (d != 0).mean() < 1e-3
     assert got[-7] == 0.0
+
+
+_SCHEDULE_SCRIPT = r"""
+import sys, json
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2302_05176_b200 as gm
+from paper_2302_05176_b200 import workloads
+ids, w, k, seed = workloads.config4(n_pairs=2_000_000, n_keys=10**7)
+rng = np.random.default_rng(5)
+w5 = rng.lognormal(0.0, 2.0, 3_000_000).astype(np.float32)
+ids5 = np.arange(w5.size, dtype=np.uint32)
+out = {}
+for name, (i, ww, kk) in {"c4": (ids, w, k), "c5": (ids5, w5, 8192)}.items():
+    y, s, em = gm.sketch_elements(i, ww, kk, gm.SeedScheme(seed))
+    out[name] = [y.cpu().numpy().tobytes().hex(), s.cpu().numpy().tobytes().hex()]
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("env", [
+    {},                                                  # default schedule
+    {"GM_ELEM_TAU_SCALE": "0.25"},                       # first walk fails, the list is re-walked / rebuilt
+    {"GM_ELEM_TAU_SCALE": "0.25", "GM_ELEM_R": "1.0"},   # list bound = tau: every failed pass streams again
+    {"GM_ELEM_TAU_SCALE": "0.5", "GM_ELEM_R": "64"},     # a wide list, several re-walks of it
+    {"GM_ELEM_FUSED": "1"},                              # fused light kernel only (overflow fallback path)
+])
+def test_elements_schedules_agree_with_oracle(env):
+    """Every K2 schedule -- first walk at tau or at the list bound, re-walks
+    of the survivor list, streaming the input again, the fused kernel --
+    gives the oracle's sketch bit for bit (s) on a config-4 Zipf prefix and a
+    config-5 prefix.  The knobs are read once per process, hence the
+    subprocess."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", _SCHEDULE_SCRIPT, root], capture_output=True, text=True,
+                         env={**os.environ, **env}, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    out = json.loads(res.stdout.strip().splitlines()[-1])
+    ids, w, k, seed = workloads.config4(n_pairs=2_000_000, n_keys=10**7)
+    rng = np.random.default_rng(5)
+    w5 = rng.lognormal(0.0, 2.0, 3_000_000).astype(np.float32)
+    ids5 = np.arange(w5.size, dtype=np.uint64)
+    for name, (i, ww, kk) in {"c4": (ids, w, k), "c5": (ids5, w5, 8192)}.items():
+        y = np.frombuffer(bytes.fromhex(out[name][0]), np.float64)
+        s = np.frombuffer(bytes.fromhex(out[name][1]), np.uint64)
+        rc, yo, so, _, _ = O.sketch_stream(i, ww.astype(np.float64), kk, seed)
+        assert rc == 0
+        assert_regs(y, s, yo, so)
