@@ -50,7 +50,7 @@ struct Workspace {
   unsigned long long* err = nullptr;       // latched data error
   unsigned long long* ull = nullptr;       // [0] heavy count, [1] emitted total
   double* dbl = nullptr;                   // [0] tau, [1] sampled weight, [2] sampled distinct weight, [3] tau_hi
-  unsigned long long* host = nullptr;      // pinned readback / upload (8 words)
+  unsigned long long* host = nullptr;      // pinned readback / upload (16 words)
   Reg* regs = nullptr;
   size_t regs_cap = 0;
   u64* heavy = nullptr;
@@ -122,7 +122,7 @@ int get_ws(cudaStream_t st, Workspace** out) {
   CK(cudaMalloc(&w->err, sizeof(unsigned long long)));
   CK(cudaMalloc(&w->ull, 4 * sizeof(unsigned long long)));
   CK(cudaMalloc(&w->dbl, 4 * sizeof(double)));
-  CK(cudaMallocHost(&w->host, 8 * sizeof(unsigned long long)));
+  CK(cudaMallocHost(&w->host, 16 * sizeof(unsigned long long)));
   CK(cudaMemset(w->counters, 0, 4 * sizeof(int)));
   CK(cudaMemset(w->err, 0, sizeof(unsigned long long)));
   CK(cudaDeviceSynchronize());
@@ -338,14 +338,16 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
                  cudaStream_t st) {
   int rc = grow(&ws->regs, &ws->regs_cap, (size_t)k, st);
   if (rc) return rc;
-  CK(cudaMemsetAsync(ws->counters, 0, 4 * sizeof(int), st));
-  CK(cudaMemsetAsync(ws->ull, 0, 4 * sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(ws->dbl, 0, 4 * sizeof(double), st));
   const unsigned rgrid = (k + 255) / 256;
-  if (flags & GM_FLAG_ACCUMULATE)
+  if (n == 0 || (flags & GM_FLAG_EXHAUSTIVE)) CK(cudaMemsetAsync(ws->ull, 0, 4 * sizeof(unsigned long long), st));
+  // fresh registers are initialised by the weight-sample launch when n > 0
+  const bool fold_init = n > 0 && !(flags & GM_FLAG_ACCUMULATE);
+  if (flags & GM_FLAG_ACCUMULATE) {
+    CK(cudaMemsetAsync(ws->counters, 0, 4 * sizeof(int), st));
     load_regs_kernel<<<rgrid, 256, 0, st>>>(ws->regs, k, y_io, s_io, ws->counters + 1);
-  else
+  } else if (!fold_init) {
     init_regs_kernel<<<rgrid, 256, 0, st>>>(ws->regs, k, ws->counters + 1);
+  }
   CK(cudaGetLastError());
   if (n > 0) {
     // blocked weight sample (~2^18 items in 1024 coalesced runs of 256)
@@ -360,7 +362,8 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
     CK(cudaMemsetAsync(ws->sample_set, 0xFF, (size_t)tcap * sizeof(unsigned long long), st));
     if ((rc = grow(&ws->sample_part, &ws->sample_part_cap, (size_t)(2 * sgrid), st))) return rc;
     weight_sample_kernel<IdT, WT><<<sgrid, 256, 0, st>>>((const IdT*)ids, (const WT*)w, n, ws->sample_set, tcap,
-                                                         ws->sample_part);
+                                                         ws->sample_part, fold_init ? ws->regs : nullptr, k,
+                                                         ws->counters + 1);
     CK(cudaGetLastError());
     const int64_t heavy_need = std::min<int64_t>(n, (int64_t)1 << 22);
     rc = grow(&ws->heavy, &ws->heavy_cap, (size_t)heavy_need, st);
@@ -384,6 +387,9 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
     const int64_t surv_cap = std::min<int64_t>(n, (int64_t)1 << 26);
     if ((rc = grow(&ws->surv, &ws->surv_cap, (size_t)surv_cap, st))) return rc;
     const int64_t fgrid = std::min<int64_t>((n / 4 + 2 * NT - 1) / (2 * NT) + 1, (int64_t)num_sms() * 8);
+    int surv_per_sm = 0;  // the list walk is latency-bound: as many resident CTAs as fit
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&surv_per_sm, elem_survivor_kernel, NT, 0));
+    surv_per_sm = std::max(surv_per_sm, 1);
     const double lk = std::log((double)k);
     double tau_h = 0.0, tau_hi_h = 0.0, R = 2.0;
     bool list_ok = false;  // the survivor list holds every element with first arrival <= tau_hi_h
@@ -410,20 +416,20 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
         CK(cudaMemcpyAsync(ws->dbl + 3, up + 1, sizeof(double), cudaMemcpyHostToDevice, st));
       } else {
         tau_kernel<<<1, 256, 0, st>>>(ws->dbl, ws->sample_part, sgrid, k, (double)n / (double)std::max<int64_t>(sampled, 1),
-                                      tau_scale, r_fixed);
+                                      tau_scale, r_fixed, ws->ull);
       }
-      CK(cudaMemsetAsync(ws->ull, 0, sizeof(unsigned long long), st));
+      if (attempt > 0 || att >= 5) CK(cudaMemsetAsync(ws->ull, 0, sizeof(unsigned long long), st));  // tau_kernel clears it at attempt 0
       bool use_filter = !fused_only && att < 4;
       for (int round = 0; round < 2; ++round) {
         if (use_filter) {
           if (rebuild) {
-            CK(cudaMemsetAsync(ws->ull + 2, 0, sizeof(unsigned long long), st));
+            if (attempt > 0 || att >= 5) CK(cudaMemsetAsync(ws->ull + 2, 0, sizeof(unsigned long long), st));
             elem_filter_kernel<IdT, WT><<<(unsigned)fgrid, NT, 0, st>>>(
                 (const IdT*)ids, (const WT*)w, n, k, useed, ws->dbl + 3, ws->surv, surv_cap,
                 ws->ull + 2, emitted_out ? ws->ull + 1 : nullptr, ws->err);
             CK(cudaGetLastError());
           }
-          elem_survivor_kernel<<<(unsigned)(num_sms() * 4), NT, 0, st>>>(
+          elem_survivor_kernel<<<(unsigned)(num_sms() * surv_per_sm), NT, 0, st>>>(
               ws->surv, ws->ull + 2, surv_cap, k, useed, pseed, ws->dbl,
               ws->regs, ws->counters + 1, ws->heavy, (int64_t)ws->heavy_cap, ws->ull,
               emitted_out ? ws->ull + 1 : nullptr);
@@ -437,11 +443,15 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
             (const IdT*)ids, (const WT*)w, use_filter ? ws->surv : nullptr, k, useed, pseed, ws->dbl, ws->regs,
             ws->counters + 1,
             ws->heavy, ws->ull, (int64_t)ws->heavy_cap, ws->dense,
-            emitted_out ? ws->ull + 1 : nullptr);
+            emitted_out ? ws->ull + 1 : nullptr, (unsigned*)(ws->counters + 2), y_io, s_io);
+        // (its last CTA stores the registers: with every attempt, a no-op
+        // rewrite when another follows, so a single-attempt call synchronises once)
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(ws->host, ws->counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(ws->host + 1, ws->ull, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(ws->host + 3, ws->ull + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ws->host + 8, ws->err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        if (emitted_out) CK(cudaMemcpyAsync(ws->host + 2, ws->ull + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         if (attempt == 0 && att < 5) CK(cudaMemcpyAsync(ws->host + 4, ws->dbl, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (attempt == 0 && att < 5) {
@@ -463,16 +473,27 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
       const unsigned long long nheavy = ws->host[1];
       if (nheavy > ws->heavy_cap)
         return fail(GM_ERR_CUDA, "internal: heavy-element list overflow (%llu > %zu)", nheavy, ws->heavy_cap);
-      if (unset == 0 || (flags & GM_FLAG_EXHAUSTIVE) || attempt >= 5) break;
+      if (unset == 0 || ws->host[8] || (flags & GM_FLAG_EXHAUSTIVE) || attempt >= 5) break;
     }
+  }
+  if (n > 0) {  // the last attempt stored the registers and read the counters back (synchronised)
+    CK(cudaGetLastError());
+    const unsigned long long e = ws->host[8];
+    if (e) {
+      CK(cudaMemsetAsync(ws->err, 0, sizeof(unsigned long long), st));
+      CK(cudaStreamSynchronize(st));
+      return map_device_error(e);
+    }
+    if (emitted_out) *emitted_out = (int64_t)ws->host[2];
+    return GM_OK;
   }
   store_regs_kernel<<<rgrid, 256, 0, st>>>(ws->regs, k, y_io, s_io);
   CK(cudaGetLastError());
-  if (emitted_out) CK(cudaMemcpyAsync(ws->host + 2, ws->ull + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(ws->host, ws->counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
   rc = check_sync(ws, st);
   if (rc) return rc;
-  if (emitted_out) *emitted_out = (int64_t)ws->host[2];
+  CK(cudaMemcpyAsync(ws->host, ws->counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (emitted_out) *emitted_out = 0;
   return GM_OK;
 }
 

@@ -259,8 +259,8 @@ __device__ __forceinline__ u32 stage_kept(u32 keep, const u64 (&idv)[NE], const 
 template <class IdT, class WT>
 __global__ void __launch_bounds__(NT, 4)
     elem_filter_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, int64_t n, u32 k, u64 useed,
-                       const double* __restrict__ tau_hi_p, Surv* __restrict__ list, int64_t cap, unsigned long long* count, unsigned long long* emitted_total,
-                       unsigned long long* err) {
+                       const double* __restrict__ tau_hi_p, Surv* __restrict__ list, int64_t cap,
+                       unsigned long long* count, unsigned long long* emitted_total, unsigned long long* err) {
   __shared__ unsigned long long cache[SURV_CACHE];
   __shared__ Surv wbuf_all[NWARP * WBUF];
   for (int i = threadIdx.x; i < SURV_CACHE; i += NT) cache[i] = ~0ull;
@@ -378,7 +378,8 @@ __global__ void __launch_bounds__(NT)
   }
 }
 
-// one warp per heavy element; dense arrays in global scratch, one per warp.
+// one warp per heavy element; dense arrays in global scratch, one per warp;
+// the last CTA stores the registers to (y_out, s_out).
 // Heavy-list entries index the survivor list when `surv` is given (after the
 // filter), the element arrays otherwise (after the fused light kernel).
 template <class IdT, class WT>
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(NT)
                       u32 k, u64 useed, u64 pseed, const double* __restrict__ tau_p, Reg* regs, int* unset_ctr,
                       const u64* __restrict__ heavy_list, const unsigned long long* heavy_count,
                       int64_t heavy_cap, u32* __restrict__ dense_global,
-                      unsigned long long* emitted_total) {
+                      unsigned long long* emitted_total, unsigned* done, double* y_out, u64* s_out) {
   __shared__ double scan_all[NWARP * 32];
   __shared__ int prov_all[NWARP * 32];
   const double tau = *tau_p;
@@ -416,6 +417,31 @@ __global__ void __launch_bounds__(NT)
   if (stamp)
     for (u32 q = lane; q < k; q += 32) dense[q] = 0;
   if (emitted_total && lane == 0 && emitted) atomicAdd(emitted_total, (unsigned long long)emitted);
+  // the last CTA to finish writes the registers out (y, s): no separate
+  // store launch; `done` is left at 0 for the next launch
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const ulonglong2* rv = reinterpret_cast<const ulonglong2*>(regs);
+  for (u32 j0 = threadIdx.x; j0 < k; j0 += 8 * NT) {  // L2 reads (the CAS results live there), 8 in flight
+    ulonglong2 r[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j0 + u * NT < k) r[u] = __ldcg(rv + j0 + u * NT);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j0 + u * NT < k) {
+        y_out[j0 + u * NT] = __longlong_as_double((long long)r[u].x);
+        s_out[j0 + u * NT] = r[u].y;
+      }
+  }
+  if (threadIdx.x == 0) *done = 0u;
 }
 
 __global__ void init_regs_kernel(Reg* regs, u32 k, int* unset_ctr) {
@@ -454,8 +480,9 @@ __global__ void store_regs_kernel(const Reg* regs, u32 k, double* y, u64* s) {
 // tau instead of streaming the input again (gm_capi.cu run_elements).
 // (one block of 256 threads; the partials are summed in a fixed order)
 __global__ void __launch_bounds__(256) tau_kernel(double* tau, const double* part, int nblocks, u32 k, double scale,
-                                                  double tau_scale, double r_fixed) {
+                                                  double tau_scale, double r_fixed, unsigned long long* ctr4) {
   __shared__ double red[2][256];
+  if (threadIdx.x < 4) ctr4[threadIdx.x] = 0ull;  // heavy count, emitted, list count, spare
   double a = 0.0, b = 0.0;
   for (int i = threadIdx.x; i < nblocks; i += 256) {
     a += part[2 * i];
@@ -493,38 +520,57 @@ __global__ void __launch_bounds__(256) tau_kernel(double* tau, const double* par
 // Blocked sample of the stream: block b of the grid reads the contiguous
 // items [b n / G, b n / G + L) (L = min(SAMPLE_RUN, n / G), coalesced), and
 // sums their weights and the weights of ids not seen before in the sample
-// (a global hash set of `tcap` slots, power of two, all ~0 on entry; a plain
-// load settles repeats of hot keys without an atomic; id ~0 is never
-// inserted and counts as new).  Per-block partials out[2b], out[2b+1];
-// tau_kernel sums them and scales by n / sampled.
+// (a global hash set of `tcap` slots, power of two, all ~0 on entry, behind a
+// run-local shared-memory set; id ~0 is never inserted and counts as new).  Per-block partials out[2b], out[2b+1];
+// tau_kernel sums them and scales by n / sampled.  With `regs` given the
+// kernel also initialises the k registers and the unset counter.
 constexpr int SAMPLE_RUN = 256;
 
 template <class IdT, class WT>
 __global__ void weight_sample_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, int64_t n,
-                                     unsigned long long* table, u32 tcap, double* out) {
+                                     unsigned long long* table, u32 tcap, double* out, Reg* regs, u32 k,
+                                     int* unset_ctr) {
+  if (regs) {  // fresh registers (one launch fewer): the grid covers any k <= 65536
+    const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < k) {
+      regs[g].y = INF_BITS;
+      regs[g].id = NO_ID;
+    }
+    if (g == 0) *unset_ctr = (int)k;
+  }
   const int64_t lo = (int64_t)blockIdx.x * n / gridDim.x;
   const int64_t hi = min(lo + (int64_t)SAMPLE_RUN, ((int64_t)blockIdx.x + 1) * n / gridDim.x);
+  // the run is first deduplicated in a shared-memory set (hot keys repeat
+  // within a run), so only the run's distinct ids go to the global set, with
+  // one atomic each (a global CAS is the cost of this kernel)
+  constexpr u32 LCAP = 2 * SAMPLE_RUN;
+  __shared__ unsigned long long lset[LCAP];
+  for (u32 i = threadIdx.x; i < LCAP; i += blockDim.x) lset[i] = ~0ull;
+  __syncthreads();
   double s = 0.0, sd = 0.0;
-  const volatile unsigned long long* vt = table;
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const double w = (double)wts[i];
     if (!(isfinite(w) && w > 0.0)) continue;
     s += w;
     const u64 id = (u64)ids[i];
     bool fresh = true;
-    if (id != ~0ull) {
-      u32 h = (u32)(mix64(id) >> 32) & (tcap - 1);
-      for (;;) {
-        if (vt[h] == (unsigned long long)id) {  // repeat of a hot key: no atomic
-          fresh = false;
-          break;
-        }
-        const unsigned long long prev = atomicCAS(&table[h], ~0ull, (unsigned long long)id);
+    if (id != ~0ull && tcap) {
+      const u64 hh = mix64(id);
+      u32 h = (u32)hh & (LCAP - 1);
+      for (;;) {  // run-local set (LCAP >= 2 x the run: always has room)
+        const unsigned long long prev = atomicCAS(&lset[h], ~0ull, (unsigned long long)id);
         if (prev == ~0ull) break;
         if (prev == (unsigned long long)id) {
           fresh = false;
           break;
         }
+        h = (h + 1) & (LCAP - 1);
+      }
+      h = (u32)(hh >> 32) & (tcap - 1);
+      while (fresh) {  // sample-wide set
+        const unsigned long long prev = atomicCAS(&table[h], ~0ull, (unsigned long long)id);
+        if (prev == ~0ull) break;
+        if (prev == (unsigned long long)id) fresh = false;
         h = (h + 1) & (tcap - 1);
       }
     }
