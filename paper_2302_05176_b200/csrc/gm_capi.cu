@@ -361,9 +361,14 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
     if ((rc = grow(&ws->sample_set, &ws->sample_set_cap, (size_t)tcap, st))) return rc;
     CK(cudaMemsetAsync(ws->sample_set, 0xFF, (size_t)tcap * sizeof(unsigned long long), st));
     if ((rc = grow(&ws->sample_part, &ws->sample_part_cap, (size_t)(2 * sgrid), st))) return rc;
+    // schedule knobs for tests (DESIGN.md 6.5): scale the first tau, fix the list ratio R
+    static const double tau_scale = getenv("GM_ELEM_TAU_SCALE") ? atof(getenv("GM_ELEM_TAU_SCALE")) : 1.0;
+    static const double r_fixed = getenv("GM_ELEM_R") ? atof(getenv("GM_ELEM_R")) : 0.0;
+    TauArgs targs{ws->dbl, ws->sample_part, sgrid, k, (double)n / (double)std::max<int64_t>(sampled, 1),
+                  tau_scale, r_fixed, ws->ull};
     weight_sample_kernel<IdT, WT><<<sgrid, 256, 0, st>>>((const IdT*)ids, (const WT*)w, n, ws->sample_set, tcap,
                                                          ws->sample_part, fold_init ? ws->regs : nullptr, k,
-                                                         ws->counters + 1);
+                                                         ws->counters + 1, targs, (unsigned*)(ws->counters + 3));
     CK(cudaGetLastError());
     const int64_t heavy_need = std::min<int64_t>(n, (int64_t)1 << 22);
     rc = grow(&ws->heavy, &ws->heavy_cap, (size_t)heavy_need, st);
@@ -381,9 +386,6 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
     // re-walks the list instead of streaming the input again.  The fused light
     // kernel serves tau = +inf, a survivor-list overflow and GM_ELEM_FUSED=1.
     static const bool fused_only = getenv("GM_ELEM_FUSED") && atoi(getenv("GM_ELEM_FUSED")) == 1;
-    // schedule knobs for tests (DESIGN.md 6.5): scale the first tau, fix the list ratio R
-    static const double tau_scale = getenv("GM_ELEM_TAU_SCALE") ? atof(getenv("GM_ELEM_TAU_SCALE")) : 1.0;
-    static const double r_fixed = getenv("GM_ELEM_R") ? atof(getenv("GM_ELEM_R")) : 0.0;
     const int64_t surv_cap = std::min<int64_t>(n, (int64_t)1 << 26);
     if ((rc = grow(&ws->surv, &ws->surv_cap, (size_t)surv_cap, st))) return rc;
     const int64_t fgrid = std::min<int64_t>((n / 4 + 2 * NT - 1) / (2 * NT) + 1, (int64_t)num_sms() * 8);
@@ -414,11 +416,8 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
         up[1] = tau_hi_h;
         CK(cudaMemcpyAsync(ws->dbl, up, sizeof(double), cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(ws->dbl + 3, up + 1, sizeof(double), cudaMemcpyHostToDevice, st));
-      } else {
-        tau_kernel<<<1, 256, 0, st>>>(ws->dbl, ws->sample_part, sgrid, k, (double)n / (double)std::max<int64_t>(sampled, 1),
-                                      tau_scale, r_fixed, ws->ull);
-      }
-      if (attempt > 0 || att >= 5) CK(cudaMemsetAsync(ws->ull, 0, sizeof(unsigned long long), st));  // tau_kernel clears it at attempt 0
+      }  // attempt 0: the sample launch set tau and tau_hi
+      if (attempt > 0 || att >= 5) CK(cudaMemsetAsync(ws->ull, 0, sizeof(unsigned long long), st));  // the sample launch clears it at attempt 0
       bool use_filter = !fused_only && att < 4;
       for (int round = 0; round < 2; ++round) {
         if (use_filter) {

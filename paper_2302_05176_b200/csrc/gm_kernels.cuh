@@ -479,14 +479,26 @@ __global__ void store_regs_kernel(const Reg* regs, u32 k, double* y, u64* s) {
 // tau that is too small, and the next pass re-walks the list with a larger
 // tau instead of streaming the input again (gm_capi.cu run_elements).
 // (one block of 256 threads; the partials are summed in a fixed order)
-__global__ void __launch_bounds__(256) tau_kernel(double* tau, const double* part, int nblocks, u32 k, double scale,
-                                                  double tau_scale, double r_fixed, unsigned long long* ctr4) {
+struct TauArgs {
+  double* tau;              // out: [0] tau, [1] W sampled, [2] W distinct, [3] tau_hi
+  const double* part;       // per-block partials of the sample
+  int nblocks;
+  u32 k;
+  double scale;             // n / sampled items
+  double tau_scale, r_fixed;  // test knobs (1, 0 by default)
+  unsigned long long* ctr4;   // cleared: heavy count, emitted, list count, spare
+};
+
+// (one block of 256 threads; the partials are summed in a fixed order)
+__device__ __forceinline__ void tau_block(const TauArgs& A) {
+  double* tau = A.tau;
+  const u32 k = A.k;
   __shared__ double red[2][256];
-  if (threadIdx.x < 4) ctr4[threadIdx.x] = 0ull;  // heavy count, emitted, list count, spare
+  if (threadIdx.x < 4) A.ctr4[threadIdx.x] = 0ull;
   double a = 0.0, b = 0.0;
-  for (int i = threadIdx.x; i < nblocks; i += 256) {
-    a += part[2 * i];
-    b += part[2 * i + 1];
+  for (int i = threadIdx.x; i < A.nblocks; i += 256) {
+    a += __ldcg(A.part + 2 * i);
+    b += __ldcg(A.part + 2 * i + 1);
   }
   red[0][threadIdx.x] = a;
   red[1][threadIdx.x] = b;
@@ -501,20 +513,20 @@ __global__ void __launch_bounds__(256) tau_kernel(double* tau, const double* par
   if (threadIdx.x) return;
   const double lk = log((double)k);
   double all = red[0][0], dist = red[1][0];
-  all *= scale;
-  dist *= scale;
+  all *= A.scale;
+  dist *= A.scale;
   tau[1] = all;
   tau[2] = dist;
   const double W = dist > 0.0 ? dist : all;
   const double ratio = (dist > 0.0 && all > dist) ? all / dist : 1.0;
-  const double R = r_fixed > 0.0 ? r_fixed : fmin(fmax(2.0 * ratio, 2.0), 256.0);
-  const double t0 = tau_scale * (lk + 3.0) / W;
+  const double R = A.r_fixed > 0.0 ? A.r_fixed : fmin(fmax(2.0 * ratio, 2.0), 256.0);
+  const double t0 = A.tau_scale * (lk + 3.0) / W;
   tau[3] = R * t0;
   // a stream with visible duplication walks the list at tau_hi right away:
   // its first tau would come from an over-estimated W, and a failed walk costs
   // a host round trip and a second walk (the list walk is ~1 arrival per
   // listed element either way)
-  tau[0] = (ratio > 1.5 && r_fixed <= 0.0) ? tau[3] : t0;
+  tau[0] = (ratio > 1.5 && A.r_fixed <= 0.0) ? tau[3] : t0;
 }
 
 // Blocked sample of the stream: block b of the grid reads the contiguous
@@ -522,14 +534,16 @@ __global__ void __launch_bounds__(256) tau_kernel(double* tau, const double* par
 // sums their weights and the weights of ids not seen before in the sample
 // (a global hash set of `tcap` slots, power of two, all ~0 on entry, behind a
 // run-local shared-memory set; id ~0 is never inserted and counts as new).  Per-block partials out[2b], out[2b+1];
-// tau_kernel sums them and scales by n / sampled.  With `regs` given the
-// kernel also initialises the k registers and the unset counter.
+// the last block sums them, scales by n / sampled and sets tau and tau_hi
+// (tau_block).  With `regs` given the kernel also initialises the k
+// registers and the unset counter.
 constexpr int SAMPLE_RUN = 256;
 
 template <class IdT, class WT>
-__global__ void weight_sample_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, int64_t n,
-                                     unsigned long long* table, u32 tcap, double* out, Reg* regs, u32 k,
-                                     int* unset_ctr) {
+__global__ void __launch_bounds__(256) weight_sample_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts,
+                                                            int64_t n, unsigned long long* table, u32 tcap, double* out,
+                                                            Reg* regs, u32 k, int* unset_ctr, TauArgs targs,
+                                                            unsigned* done) {
   if (regs) {  // fresh registers (one launch fewer): the grid covers any k <= 65536
     const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g < k) {
@@ -588,7 +602,8 @@ __global__ void weight_sample_kernel(const IdT* __restrict__ ids, const WT* __re
     red[1][warp] = sd;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // per-block partials, summed in block order by tau_kernel (deterministic)
+  __shared__ bool last;
+  if (threadIdx.x == 0) {  // per-block partials, summed in block order by the last block (deterministic)
     double a = 0.0, b = 0.0;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
       a += red[0][i];
@@ -596,7 +611,14 @@ __global__ void weight_sample_kernel(const IdT* __restrict__ ids, const WT* __re
     }
     out[2 * blockIdx.x] = a;
     out[2 * blockIdx.x + 1] = b;
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
   }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  tau_block(targs);  // the pass threshold and the list bound (one launch fewer)
+  if (threadIdx.x == 0) *done = 0u;
 }
 
 __global__ void merge_kernel(const double* __restrict__ y_in, const u64* __restrict__ s_in,
