@@ -366,9 +366,9 @@ def run_ours_elements(args, rank, world, local_rank):
         "e2e": {"value": n_all / (e2e_ms / 1e3), "unit": "elements/s", "h2d_bytes_per_step": in_bytes,
                 "d2h_bytes_per_step": 16 * k, "ms_per_step": e2e_ms,
                 "api": "gm_sketch_elements_host (pinned host buffers), wall clock"},
-        "gpu_launches": 7 * args.steps + (args.steps if world > 1 else 0),
-        "gpu_launches_note": "per sketch: init, weight sample, tau, filter, survivor walk, heavy walk, store "
-                             "(+ merge for N > 1) when the first walk completes every register",
+        "gpu_launches": 4 * args.steps + (args.steps if world > 1 else 0),
+        "gpu_launches_note": "per sketch: weight sample (+ register init, tau), filter, survivor walk, heavy walk "
+                             "(+ register store) -- and the merge for N > 1 -- when the first walk completes every register",
         "roofline": {"bound": "hbm", "unit": "GB/s", "achieved": achieved, "peak": hbm_peak, "frac": achieved / hbm_peak,
                      "traffic": traffic, "peak_kind": hbm_kind,
                      "achieved_note": "input bytes (ids + weights) per sketch / whole sketch step (all its kernels)"},
