@@ -14,6 +14,10 @@ Outputs (committed):
   config1.npz         BASELINE config 1 (ids 0..9999, w = 1 - default_rng(1).random,
                       k=256, seed 1) via sketch_stream (ids include 0)
   config2_sample.npz  first 4 vectors of the config-2 generator via sketch_fast
+  wire_records.json   sketch_to_json records (sketch.py:325-339) of the first 8
+                      sketch_cases vectors' sketch_fast sketches and of one merge
+
+Only the wire records:  python tests/golden/make_golden.py wire
 """
 
 from __future__ import annotations
@@ -182,13 +186,43 @@ def config2_sample():
                         emitted=np.array(ems, np.int64))
 
 
+def wire_records():
+    """The reference's own serialisation of sketches built from the
+    sketch_cases inputs (bit-exact hex floats)."""
+    with open(os.path.join(HERE, "sketch_cases.json")) as f:
+        cases = json.load(f)["vectors"]
+    out = []
+    sks = []
+    for c in cases[:8]:
+        v = G.WeightedVector({e: float.fromhex(w) for e, w in zip(c["ids"], c["w"])})
+        sk = G.sketch_fast(v, G.GenerationParams(k=c["k"], scheme=G.SeedScheme(c["seed"])))
+        out.append({"case": cases.index(c), "record": G.sketch_to_json(sk)})
+        sks.append(sk)
+    # a merge of two sketches of the same k and scheme (estimate.py:103-125)
+    rng = random.Random(7)
+    a = G.WeightedVector({rng.randrange(1, 10**6): rng.random() + 1e-9 for _ in range(50)})
+    b = G.WeightedVector({rng.randrange(1, 10**6): rng.random() + 1e-9 for _ in range(70)})
+    p = G.GenerationParams(k=32, scheme=G.SeedScheme(99))
+    m = G.merge([G.sketch_fast(a, p), G.sketch_fast(b, p)])
+    out.append({"merge": {"a": [[e, w.hex()] for e, w in a.items()], "b": [[e, w.hex()] for e, w in b.items()],
+                          "k": 32, "seed": 99}, "record": G.sketch_to_json(m)})
+    return out
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["wire"]:
+        with open(os.path.join(HERE, "wire_records.json"), "w") as f:
+            json.dump(wire_records(), f, indent=0)
+        print("wire records written")
+        sys.exit(0)
     with open(os.path.join(HERE, "rng_kats.json"), "w") as f:
         json.dump(rng_kats(), f)
     with open(os.path.join(HERE, "sketch_cases.json"), "w") as f:
         json.dump(sketch_cases(), f)
     with open(os.path.join(HERE, "bench_golden.json"), "w") as f:
         json.dump(bench_golden(), f, indent=1)
+    with open(os.path.join(HERE, "wire_records.json"), "w") as f:
+        json.dump(wire_records(), f, indent=0)
     config1()
     config2_sample()
     print("golden fixtures written to", HERE)

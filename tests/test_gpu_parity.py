@@ -671,3 +671,36 @@ def test_elements_schedules_agree_with_oracle(env):
         rc, yo, so, _, _ = O.sketch_stream(i, ww.astype(np.float64), kk, seed)
         assert rc == 0
         assert_regs(y, s, yo, so)
+
+
+def test_device_sketches_serialise_to_reference_records():
+    """End to end through the wire format: sketch_fast on the device (exact-y
+    finalize) and merge, serialised with sketch_to_json, give byte-for-byte the
+    records the reference wrote for the same inputs (tests/golden/wire_records.json),
+    so device-built sketches interoperate with the reference's CLI and service files."""
+    cases = load_json("sketch_cases.json")["vectors"]
+    for rec in load_json("wire_records.json"):
+        if "case" in rec:
+            c = cases[rec["case"]]
+            ids, w = vector_case(c)
+            v = gm.WeightedVector({int(e): float(x) for e, x in zip(ids, w)})
+            sk = gm.sketch_fast(v, gm.GenerationParams(k=c["k"], scheme=gm.SeedScheme(c["seed"])))
+        else:
+            m = rec["merge"]
+            p = gm.GenerationParams(k=m["k"], scheme=gm.SeedScheme(m["seed"]))
+            a = gm.WeightedVector({e: float.fromhex(x) for e, x in m["a"]})
+            b = gm.WeightedVector({e: float.fromhex(x) for e, x in m["b"]})
+            sk = gm.merge([gm.sketch_fast(a, p), gm.sketch_fast(b, p)])
+        assert gm.sketch_to_json(sk) == rec["record"]
+
+
+def test_empty_element_set_is_incomplete():
+    """No elements leave every register unset: IncompleteSketchError, as
+    stream_finalize raises for an empty stream (stream.py:132-134); folded
+    into an existing complete sketch (accumulate) an empty set is a no-op."""
+    with pytest.raises(gm.IncompleteSketchError):
+        gm.sketch_elements(np.zeros(0, np.uint32), np.zeros(0, np.float32), 64, gm.SeedScheme(1))
+    y, s, _ = gm.sketch_elements(np.arange(1, 500, dtype=np.uint32), np.ones(499, np.float32), 64, gm.SeedScheme(1))
+    y2, s2 = y.clone(), s.clone()
+    gm.sketch_elements(np.zeros(0, np.uint32), np.zeros(0, np.float32), 64, gm.SeedScheme(1), into=(y2, s2))
+    assert torch.equal(y, y2) and torch.equal(s, s2)

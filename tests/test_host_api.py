@@ -153,3 +153,20 @@ def test_shard_vector_ranges_balance_elements():
         assert rs[0][0] == 0 and rs[-1][1] == sizes.size
         loads = [int(off[b] - off[a]) for a, b in rs]
         assert max(loads) <= off[-1] / world + sizes.max()
+
+
+def test_wire_records_match_reference_bytes():
+    """sketch_to_json / sketch_from_json (sketch.py:325-357) against records
+    the reference itself wrote (tests/golden/wire_records.json): the sketches
+    of the golden sketch_cases (sketch_fast) and a merge, rebuilt from the
+    fixture values, serialise to the same bytes and parse back equal."""
+    cases = load_json("sketch_cases.json")["vectors"]
+    for rec in load_json("wire_records.json"):
+        if "case" in rec:
+            c = cases[rec["case"]]["fast"]
+            k = cases[rec["case"]]["k"]
+            sk = gm.GumbelMaxSketch(k, tuple(int(x) for x in c["s"]), tuple(float.fromhex(v) for v in c["y"]),
+                                    int(c["fingerprint"]))
+            assert gm.sketch_to_json(sk) == rec["record"]
+        back = gm.sketch_from_json(rec["record"])
+        assert gm.sketch_to_json(back) == rec["record"]
