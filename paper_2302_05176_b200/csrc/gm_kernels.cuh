@@ -124,13 +124,18 @@ __global__ void __launch_bounds__(NT)
 // log, no divide, no MUFU and no fp64: with h23 the top 23 bits of the
 // uniform hash, u1 = (h >> 11) 2^-53 + 2^-54 <= (h23 + 1) 2^-23, and
 // e^-x >= 1 - x, so the element is skipped when
-//   (h23 + 1) < A (1 - x),  A = 2^23 (1 - 2^-12),  x = tau_hi k w,
+//   (h23 + 1) < A (1 - x),  A = 2^23 (1 - 2^-16),  x = tau_hi k w,
 // evaluated as  float(2^23 + h23) < fma(x, -A, A + 2^23 - 1)  (the left side
 // is the bit pattern 0x4B000000 | h23, exact).  Error budget: x carries
-// <= 2e-7 relative error (two fp32 roundings), the fma rounds by <= 0.5 (the
-// result is below 2^24, ulp 1); both stay inside the 2^-12 margin (an
-// effective 2^-13 in the log domain for every x), so an element
-// is skipped only if its exact fp64 first arrival exceeds tau_hi.  For x
+// <= 1.2e-7 relative error (two fp32 roundings), the fma rounds by <= 0.5
+// (the result is below 2^24, ulp <= 1), so a skip implies
+// (h23 + 1) 2^-23 < (1 - 2^-16)(1 - x) + 1.2e-7 x + 2^-24 <= (1 - 2^-17) e^-x
+// (for x <= 1/2, 2^-17 (1 - x) >= 3.8e-6 exceeds 1.2e-7 x + 2^-24; beyond,
+// e^-x - 1 + x >= 0.1 absorbs them): the element's exact first arrival exceeds
+// tau_hi by -log(1 - 2^-17) / (w k) ~ 7.6e-6 / (w k), far beyond fp64
+// rounding, so it is skipped only if its exact fp64 first arrival exceeds
+// tau_hi.  The margin
+// keeps a fraction 2^-16 of the elements whatever their arrival.  For x
 // beyond ~1 the right side drops below 2^23 and the element is kept (the
 // exact walk decides).  mix64's final xor-shift leaves bits 41..63 unchanged,
 // so the last shift is not computed.  Survivors (~k (ln k + c) tau_hi / tau
@@ -143,8 +148,8 @@ __device__ __forceinline__ u32 mix64_hi23(u64 x) {
   return (u32)((x * M2) >> 41);
 }
 
-constexpr float FILTER_A = 8388608.0f * (1.0f - 0x1p-12f);           // 2^23 (1 - 2^-12)
-constexpr float FILTER_B = 8388608.0f * (1.0f - 0x1p-12f) + 8388607.0f;  // A + 2^23 - 1 (exact)
+constexpr float FILTER_A = 8388608.0f * (1.0f - 0x1p-16f);           // 2^23 (1 - 2^-16) = 2^23 - 2^7
+constexpr float FILTER_B = 8388608.0f * (1.0f - 0x1p-16f) + 8388607.0f;  // A + 2^23 - 1 (exact, < 2^24)
 
 __device__ __forceinline__ bool filter_skip_f(u64 key, float x) {  // key = useed + id K_ELEM + K_STEP
   return __uint_as_float(0x4B000000u | mix64_hi23(key)) < __fmaf_rn(x, -FILTER_A, FILTER_B);
