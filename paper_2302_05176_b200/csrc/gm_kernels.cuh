@@ -538,11 +538,12 @@ __device__ __forceinline__ void tau_block(const TauArgs& A) {
 // items [b n / G, b n / G + L) (L = min(SAMPLE_RUN, n / G), coalesced), and
 // sums their weights and the weights of ids not seen before in the sample
 // (a global hash set of `tcap` slots, power of two, all ~0 on entry, behind a
-// run-local shared-memory set; id ~0 is never inserted and counts as new).  Per-block partials out[2b], out[2b+1];
+// run-local shared-memory set, and used only by runs that repeat an id
+// themselves; id ~0 is never inserted and counts as new).  Per-block partials out[2b], out[2b+1];
 // the last block sums them, scales by n / sampled and sets tau and tau_hi
 // (tau_block).  With `regs` given the kernel also initialises the k
 // registers and the unset counter.
-constexpr int SAMPLE_RUN = 256;
+constexpr int SAMPLE_RUN = 256;  // <= the launch's 256 threads: one item per thread
 
 template <class IdT, class WT>
 __global__ void __launch_bounds__(256) weight_sample_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts,
@@ -566,35 +567,46 @@ __global__ void __launch_bounds__(256) weight_sample_kernel(const IdT* __restric
   __shared__ unsigned long long lset[LCAP];
   for (u32 i = threadIdx.x; i < LCAP; i += blockDim.x) lset[i] = ~0ull;
   __syncthreads();
+  // one item per thread (SAMPLE_RUN <= blockDim.x)
   double s = 0.0, sd = 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+  const int64_t i = lo + threadIdx.x;
+  bool fresh = false;
+  u64 id = 0, hh = 0;
+  if (i < hi) {
     const double w = (double)wts[i];
-    if (!(isfinite(w) && w > 0.0)) continue;
-    s += w;
-    const u64 id = (u64)ids[i];
-    bool fresh = true;
-    if (id != ~0ull && tcap) {
-      const u64 hh = mix64(id);
-      u32 h = (u32)hh & (LCAP - 1);
-      for (;;) {  // run-local set (LCAP >= 2 x the run: always has room)
-        const unsigned long long prev = atomicCAS(&lset[h], ~0ull, (unsigned long long)id);
-        if (prev == ~0ull) break;
-        if (prev == (unsigned long long)id) {
-          fresh = false;
-          break;
+    if (isfinite(w) && w > 0.0) {
+      s = w;
+      fresh = true;
+      id = (u64)ids[i];
+      if (id != ~0ull && tcap) {
+        hh = mix64(id);
+        u32 h = (u32)hh & (LCAP - 1);
+        for (;;) {  // run-local set (LCAP >= 2 x the run: always has room)
+          const unsigned long long prev = atomicCAS(&lset[h], ~0ull, (unsigned long long)id);
+          if (prev == ~0ull) break;
+          if (prev == (unsigned long long)id) {
+            fresh = false;
+            break;
+          }
+          h = (h + 1) & (LCAP - 1);
         }
-        h = (h + 1) & (LCAP - 1);
-      }
-      h = (u32)(hh >> 32) & (tcap - 1);
-      while (fresh) {  // sample-wide set
-        const unsigned long long prev = atomicCAS(&table[h], ~0ull, (unsigned long long)id);
-        if (prev == ~0ull) break;
-        if (prev == (unsigned long long)id) fresh = false;
-        h = (h + 1) & (tcap - 1);
       }
     }
-    if (fresh) sd += w;
   }
+  // a run without any repeat goes no further (a stream without duplicates
+  // then costs no global atomics); a run with repeats checks its distinct ids
+  // against the sample-wide set
+  const bool run_dups = __syncthreads_or(s > 0.0 && !fresh);
+  if (run_dups && fresh && id != ~0ull && tcap) {
+    u32 h = (u32)(hh >> 32) & (tcap - 1);
+    while (fresh) {  // sample-wide set
+      const unsigned long long prev = atomicCAS(&table[h], ~0ull, (unsigned long long)id);
+      if (prev == ~0ull) break;
+      if (prev == (unsigned long long)id) fresh = false;
+      h = (h + 1) & (tcap - 1);
+    }
+  }
+  if (fresh) sd = s;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
