@@ -566,7 +566,7 @@ def run_ours(args, rank, world, local_rank):
         n_sample = int(min(n_vec, max(threads, 15.0 / max(dt_probe / 64, 1e-9))))
         dt, n = cpu_oracle_time(ids, w, off, k, seed, n_sample, threads)
         cpu = {"value": n / dt, "unit": "elements/s", "cores": threads, "kind": "port",
-               "sample": f"first {n_sample} of {n_vec} config-2 vectors ({n} elements), "
+               "sample": f"first {n_sample} of {n_vec} config-{args.config} vectors ({n} elements), "
                          "oracle/gm_oracle.c sketch_fast, all host threads"}
 
     line = {
