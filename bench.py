@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5])
     p.add_argument("--n", type=float, default=0, help="configs 4/5: override the element count (default: BASELINE size)")
+    p.add_argument("--merge", default="allgather", choices=["allgather", "allreduce"],
+                   help="configs 4/5, N > 1: all-gather + rank-order device merge, or two MIN all-reduces")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--streams", type=int, default=6, help="CUDA streams the batches rotate over")
     return p.parse_args()
@@ -277,6 +279,8 @@ def run_ours_elements(args, rank, world, local_rank):
         if rc:
             raise RuntimeError(_lib.last_error())
         if world > 1:
+            if args.merge == "allreduce":
+                return shard.allreduce_min_registers(y, s)
             return shard.merge_across_ranks(y, s)
         return y, s
 
@@ -361,7 +365,8 @@ def run_ours_elements(args, rank, world, local_rank):
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, workloads.py)",
         "config": {"workload": desc, "elements_per_step": n_all, "k": k,
-                   "parallelism": f"element shards x{world} + NCCL all-gather/device merge" if world > 1 else "single GPU",
+                   "parallelism": (f"element shards x{world} + NCCL " + ("MIN all-reduces" if args.merge == "allreduce"
+                                   else "all-gather + device merge")) if world > 1 else "single GPU",
                    "l2": f"inputs ({(ids.nbytes + w.nbytes) >> 20} MiB) larger than the 126 MB L2"},
         "e2e": {"value": n_all / (e2e_ms / 1e3), "unit": "elements/s", "h2d_bytes_per_step": in_bytes,
                 "d2h_bytes_per_step": 16 * k, "ms_per_step": e2e_ms,

@@ -8,6 +8,10 @@ Two shapes, SURVEY.md section 8(e):
     registers (k x 16 B) and min-merges them in rank order with the device
     merge kernel, which reproduces merge([sketch_rank0, sketch_rank1, ...])
     exactly (estimate.py:103-125; partition law test_estimate.py:174-199).
+    `allreduce_min_registers` is the collective-only alternative: two
+    all-reduces with MIN (y, then the ids of the registers that hold the
+    minimum), the register-wise lexicographic (y, id) minimum -- the whole
+    element set's sketch (sketch_naive's smaller-id tie rule, sketch.py:196-205).
 """
 
 from __future__ import annotations
@@ -56,3 +60,23 @@ def merge_across_ranks(y: torch.Tensor, s: torch.Tensor, group=None) -> tuple[to
 
     ya, sa = gather_registers(y, s, group)
     return merge_arrays(ya, sa)
+
+
+_SIGN = 1 << 63
+
+
+def allreduce_min_registers(y: torch.Tensor, s: torch.Tensor, group=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Every rank ends with the register-wise lexicographic minimum of
+    (y, s) over the ranks: all-reduce(MIN) of y, then all-reduce(MIN) of the
+    ids of the ranks that hold that minimum (others contribute the largest
+    id).  Ids are unsigned 64-bit values carried in int64: the sign bit is
+    flipped so that signed MIN orders them as unsigned.  Equal to the
+    rank-order merge unless two ranks hold different elements with the very
+    same y bits in one register (then the smaller id wins, as in
+    sketch_naive over the whole set)."""
+    ym = y.clone()
+    dist.all_reduce(ym, op=dist.ReduceOp.MIN, group=group)
+    sign = torch.tensor(-_SIGN, dtype=torch.int64, device=s.device)  # bit pattern 1 << 63
+    key = torch.where(y == ym, s ^ sign, torch.full_like(s, (1 << 63) - 1))
+    dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)
+    return ym, key ^ sign

@@ -38,7 +38,8 @@ def _stream_worker(rank, port, out_dir):
     assert rc == 0
     ya, sa = shard.gather_registers(torch.from_numpy(y), torch.from_numpy(s.view(np.int64)))
     ym, sm = O.merge(ya.numpy(), sa.numpy().view(np.uint64))
-    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), y=ym, s=sm)
+    yr, sr = shard.allreduce_min_registers(torch.from_numpy(y.copy()), torch.from_numpy(s.view(np.int64).copy()))
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), y=ym, s=sm, yr=yr.numpy(), sr=sr.numpy().view(np.uint64))
     dist.destroy_process_group()
 
 
@@ -68,6 +69,9 @@ def test_stream_shards_merge_to_whole(tmp_path):
         d = np.load(tmp_path / f"rank{r}.npz")
         assert np.array_equal(d["s"], sw)
         assert d["y"].tolist() == yw.tolist()
+        # the MIN all-reduce variant gives the same registers
+        assert np.array_equal(d["sr"], sw)
+        assert d["yr"].tolist() == yw.tolist()
 
 
 @pytest.mark.timeout(300)
@@ -80,3 +84,26 @@ def test_vector_shards_cover_batch(tmp_path):
     y = np.concatenate([p["y"] for p in parts])
     s = np.concatenate([p["s"] for p in parts])
     assert np.array_equal(s, sw) and y.tolist() == yw.tolist()
+
+
+def _minreduce_worker(rank, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    # hand-made registers: ids above 2**63 (negative as int64), exact y ties
+    # between ranks (smaller id wins), unset registers (inf, id 2**64-1)
+    inf = float("inf")
+    y = [[1.0, 2.0, inf, 3.0, 5.0], [1.0, 1.5, inf, 3.0, inf]][rank]
+    s = [[(1 << 64) - 2, 7, (1 << 64) - 1, (1 << 63) + 5, 9], [(1 << 63), 8, (1 << 64) - 1, (1 << 63) + 4, (1 << 64) - 1]][rank]
+    yr, sr = shard.allreduce_min_registers(torch.tensor(y, dtype=torch.float64),
+                                           torch.from_numpy(np.array(s, dtype=np.uint64).view(np.int64)))
+    np.savez(os.path.join(out_dir, f"mr{rank}.npz"), y=yr.numpy(), s=sr.numpy().view(np.uint64))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_allreduce_min_unsigned_ids_and_ties(tmp_path):
+    mp.spawn(_minreduce_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, join=True)
+    for r in range(WORLD):
+        d = np.load(tmp_path / f"mr{r}.npz")
+        assert d["y"].tolist() == [1.0, 1.5, float("inf"), 3.0, 5.0]
+        assert d["s"].tolist() == [1 << 63, 8, (1 << 64) - 1, (1 << 63) + 4, 9]
