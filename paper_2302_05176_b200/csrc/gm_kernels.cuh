@@ -235,8 +235,24 @@ __device__ __noinline__ void flush_kept(const Surv* wbuf, u32 wcount, Surv* list
   __syncwarp();
 }
 
+// a[e] for a register array and a run-time e, as a select tree (indexing a
+// register array with a run-time index would put it in local memory)
+template <int NE, class T>
+__device__ __forceinline__ T pick(const T (&a)[NE], int e) {
+  if constexpr (NE == 1) {
+    return a[0];
+  } else {
+    static_assert(NE == 8, "pick: 1 or 8 entries");
+    const T l0 = (e & 1) ? a[1] : a[0], l1 = (e & 1) ? a[3] : a[2];
+    const T l2 = (e & 1) ? a[5] : a[4], l3 = (e & 1) ? a[7] : a[6];
+    const T m0 = (e & 2) ? l1 : l0, m1 = (e & 2) ? l3 : l2;
+    return (e & 4) ? m1 : m0;
+  }
+}
+
 // stage the kept elements of one iteration (bit e of keep: idv[e], wv[e]);
-// returns the warp's new staged count
+// returns the warp's new staged count.  Lanes loop over their set bits only
+// (a lane keeps one or two of its eight elements at a time).
 template <int NE, class WV>
 __device__ __forceinline__ u32 stage_kept(u32 keep, const u64 (&idv)[NE], const WV (&wv)[NE], Surv* wbuf,
                                           u32 wcount, Surv* list, int64_t cap, unsigned long long* count,
@@ -255,9 +271,10 @@ __device__ __forceinline__ u32 stage_kept(u32 keep, const u64 (&idv)[NE], const 
     wcount = 0;
   }
   u32 pos = wcount + incl - c;
-#pragma unroll
-  for (int e = 0; e < NE; ++e)
-    if ((keep >> e) & 1u) wbuf[pos++] = Surv{idv[e], (double)wv[e]};
+  for (u32 m = keep; m; m &= m - 1, ++pos) {
+    const int e = __ffs(m) - 1;
+    wbuf[pos] = Surv{pick(idv, e), (double)pick(wv, e)};
+  }
   return wcount + total;
 }
 
@@ -311,11 +328,13 @@ __global__ void __launch_bounds__(NT, 4)
       u32 keep = okm & ~skm;
       const u32 bad = ~okm & 0xFFu;
       skipped += __popc(okm & skm);
-      if (keep) {  // drop ids this CTA has listed already (hot stream keys)
+      if (keep) {  // drop ids this CTA has listed already (hot stream keys): set bits only
         const volatile unsigned long long* vc = cache;
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (((keep >> e) & 1u) && vc[surv_slot(idv[e])] == (unsigned long long)idv[e]) keep &= ~(1u << e);
+        for (u32 m = keep; m; m &= m - 1) {
+          const int e = __ffs(m) - 1;
+          const u64 id = pick(idv, e);
+          if (vc[surv_slot(id)] == (unsigned long long)id) keep &= ~(1u << e);
+        }
       }
       // bit e: quad q0 (e < 4) or q1 (e >= 4), element e & 3
       if (__any_sync(0xFFFFFFFFu, keep != 0u))
