@@ -319,21 +319,41 @@ __global__ void __launch_bounds__(NT, 4)
       }
       const float4 w0 = __ldcs(&wq[q0]), w1 = __ldcs(&wq[q1]);
       const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-      u32 okm = 0, skm = 0;
+      u32 keep, bad = 0;
+      if constexpr (sizeof(IdT) == 4) {
+        // skip = the test passes and w > 0: a zero, negative, infinite or NaN
+        // weight is never skipped (the fma gives -inf or NaN for the last two),
+        // so weights are validated on the kept elements only.  (With u64 ids
+        // the extra live values of that path spill at the 64-register budget:
+        // there every weight is validated up front.)
+        u32 skm = 0;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        okm |= (u32)weight_ok_f32(wv[e]) << e;
-        skm |= (u32)filter_skip_f(c0 + idv[e] * K_ELEM, tkf * wv[e]) << e;
+        for (int e = 0; e < 8; ++e)
+          skm |= (u32)(filter_skip_f(c0 + idv[e] * K_ELEM, tkf * wv[e]) & (wv[e] > 0.0f)) << e;
+        keep = ~skm & 0xFFu;
+        skipped += __popc(skm);
+      } else {
+        u32 okm = 0, skm = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          okm |= (u32)weight_ok_f32(wv[e]) << e;
+          skm |= (u32)filter_skip_f(c0 + idv[e] * K_ELEM, tkf * wv[e]) << e;
+        }
+        keep = okm & ~skm;
+        bad = ~okm & 0xFFu;
+        skipped += __popc(okm & skm);
       }
-      u32 keep = okm & ~skm;
-      const u32 bad = ~okm & 0xFFu;
-      skipped += __popc(okm & skm);
-      if (keep) {  // drop ids this CTA has listed already (hot stream keys): set bits only
+      if (keep) {  // (validate;) drop ids this CTA has listed already (hot stream keys): set bits only
         const volatile unsigned long long* vc = cache;
         for (u32 m = keep; m; m &= m - 1) {
           const int e = __ffs(m) - 1;
           const u64 id = pick(idv, e);
-          if (vc[surv_slot(id)] == (unsigned long long)id) keep &= ~(1u << e);
+          if (sizeof(IdT) == 4 && !weight_ok_f32(pick(wv, e))) {
+            bad |= 1u << e;
+            keep &= ~(1u << e);
+          } else if (vc[surv_slot(id)] == (unsigned long long)id) {
+            keep &= ~(1u << e);
+          }
         }
       }
       // bit e: quad q0 (e < 4) or q1 (e >= 4), element e & 3

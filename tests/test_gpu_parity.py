@@ -704,3 +704,18 @@ def test_empty_element_set_is_incomplete():
     y2, s2 = y.clone(), s.clone()
     gm.sketch_elements(np.zeros(0, np.uint32), np.zeros(0, np.float32), 64, gm.SeedScheme(1), into=(y2, s2))
     assert torch.equal(y, y2) and torch.equal(s, s2)
+
+
+@pytest.mark.parametrize("bad", [0.0, -1.0, float("nan"), float("inf"), -0.0])
+@pytest.mark.parametrize("id_dtype", [np.uint32, np.uint64])
+def test_elements_bad_weight_anywhere_raises(bad, id_dtype):
+    """A weight that is not finite and > 0 anywhere in a large element set
+    (the vectorised filter path, where u32-id weights are validated only on
+    elements the filter keeps) raises InvalidWeightError (stream.py:63-66)."""
+    n = 1 << 20
+    rng = np.random.default_rng(17)
+    w = rng.exponential(1.0, n).astype(np.float32) + np.float32(1e-3)
+    ids = np.arange(n, dtype=id_dtype) * 7 + 1
+    w[654_321] = np.float32(bad)
+    with pytest.raises(gm.InvalidWeightError):
+        gm.sketch_elements(ids, w, 1024, gm.SeedScheme(3))
