@@ -19,9 +19,10 @@ its 8 MB of input in and its 16 MB of registers out).
 vector (1e9 elements, k=8192) per step; N > 1 shards the elements and merges
 the per-rank sketches (strong scaling).
 
-N > 1 (torchrun): vectors are sharded across ranks by element count, no
-collective on the data path (scaling "weak": every rank sketches its own
-full config-2 batch); timing is max over ranks of device time.
+N > 1 (torchrun): config 2 scales weakly (every rank sketches its own full
+batch); config 3 strongly (its vectors are split into contiguous ranges
+balanced by element count); no collective on the data path; timing is max
+over ranks of device time.
 
 --impl reference times the reference algorithm's CPU implementation (the
 bit-exact C port of sketch_fast in oracle/, all host threads) on the same
@@ -398,9 +399,19 @@ def run_ours(args, rank, world, local_rank):
     L = _lib.load()
     ids, w, off, k, seed, desc = load_workload(args.config)
     scheme = gm.SeedScheme(seed)
-    # weak scaling: every rank sketches a full batch of its own; at N=1 this is the config
+    # config 2: weak scaling, every rank sketches a full batch of its own (at N=1
+    # this is the config); config 3: strong scaling, the 1e5 vectors are split
+    # into contiguous ranges balanced by element count (shard.vector_ranges),
+    # no collective on the data path
+    n_all = int(off[-1])
+    strong = args.config == 3 and world > 1
+    if strong:
+        v0, v1 = shard.vector_ranges(off, world)[rank]
+        lo_e, hi_e = int(off[v0]), int(off[v1])
+        ids, w, off = ids[lo_e:hi_e], w[lo_e:hi_e], off[v0:v1 + 1] - lo_e
     n_vec = off.size - 1
     n_el = int(off[-1])
+    n_job = n_all if strong else n_el * world  # elements the whole job sketches per step
     # Batches stream through NSTREAMS CUDA streams in turn, so one batch's
     # first CTAs and input copy overlap the previous batch's tail (a batch
     # ends with a ramp-down in which most SMs are idle).  Inputs
@@ -462,7 +473,7 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
         dist.barrier()
-    value = n_el * world * args.steps / (total_ms / 1e3)
+    value = n_job * args.steps / (total_ms / 1e3)
 
     # one batch alone on an idle GPU (L2 flushed first): the latency figure
     lat = []
@@ -510,7 +521,7 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
-    e2e_value = n_el * world * args.steps / (e2e_total / 1e3)
+    e2e_value = n_job * args.steps / (e2e_total / 1e3)
     h2d = ids.nbytes + w.nbytes + off.nbytes
     d2h = n_vec * k * 12  # y f64 + s u32
 
@@ -577,10 +588,11 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": "positive elements sketched/sec at k=%d" % k,
         "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, workloads.py)",
         "config": {"workload": desc, "elements_per_step_per_gpu": n_el, "k": k,
-                   "parallelism": f"vector shards x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"vector shards x{world} balanced by elements" if strong else
+                                   f"a full batch per rank x{world}") if world > 1 else "single GPU",
                    "batches": f"a stream of batches over {ns} CUDA streams (consecutive batches overlap)",
                    "l2": f"inputs rotated over {N_COPIES} resident copies ({N_COPIES * (ids.nbytes + w.nbytes) >> 20} MiB > 126 MB L2)",
                    "batch_latency_ms": batch_ms,
