@@ -407,6 +407,12 @@ __global__ void __launch_bounds__(NT)
   u32* mymap = maps + threadIdx.x;
   for (int64_t j = (int64_t)blockIdx.x * NT + threadIdx.x; j < m; j += (int64_t)gridDim.x * NT) {
     const Surv v = list[j];
+    // the list was built for tau_hi >= tau: the filter's fp32 test against this
+    // pass's tau drops most entries beyond it without the exact arithmetic
+    if (filter_skip_f(useed + K_STEP + v.id * K_ELEM, (float)(tau * (double)k * v.w)) & (v.w > 0.0)) {
+      emitted += 1;
+      continue;
+    }
     bool ok = false;
     if (v.w < light_w) ok = walk_light<false>(v.id, v.w, tau, k, useed, pseed, mymap, NT, 16, regs, unset_ctr, emitted);
     if (!ok) {

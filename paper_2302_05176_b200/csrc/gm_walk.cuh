@@ -38,12 +38,13 @@ __device__ __forceinline__ bool walk_light(u64 id, double w, double tau, u32 k, 
                                            int* unset_ctr, u32& emitted) {
   const u64 ubase = useed + id * K_ELEM;
   const u64 pbase = pseed + id * K_ELEM;
+  const bool fast = w_fast(w);  // the branch-free divide gives the IEEE quotient in this range
   double b = 0.0;
   int nl = 0;
   u32 z = 0;
   while (z < k) {
     ++z;
-    const double t = __dadd_rn(b, spacing(ubase, z, w, k));
+    const double t = __dadd_rn(b, fast ? spacing_t<true>(ubase, z, w, k) : spacing_t<false>(ubase, z, w, k));
     if (t > tau) break;
     b = t;
     const u32 j = perm_draw(pbase, z, k);
