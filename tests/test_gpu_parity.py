@@ -719,3 +719,21 @@ def test_elements_bad_weight_anywhere_raises(bad, id_dtype):
     w[654_321] = np.float32(bad)
     with pytest.raises(gm.InvalidWeightError):
         gm.sketch_elements(ids, w, 1024, gm.SeedScheme(3))
+
+
+@pytest.mark.parametrize("n", [1, 3, 100, 1000, 5000])
+@pytest.mark.parametrize("k", [1, 2, 64, 4096])
+def test_elements_small_sets_with_repeats(n, k):
+    """Small element sets (the sample covers every item, runs shorter than a
+    block, the scalar filter path) with repeated ids of equal weight and ids
+    near 2**64, against the oracle's stream sketch (repeats are no-ops)."""
+    rng = np.random.default_rng(1000 * n + k)
+    base = rng.integers(0, 1 << 63, size=max(1, n // 2), dtype=np.uint64) * np.uint64(2) + np.uint64(1)
+    base[0] = np.uint64((1 << 64) - 1)
+    wb = rng.lognormal(0.0, 1.0, base.size).astype(np.float32)
+    pick = rng.integers(0, base.size, size=n)
+    ids, w = base[pick], wb[pick]
+    y, s, _ = gm.sketch_elements(ids, w, k, gm.SeedScheme(77))
+    rc, yo, so, _, _ = O.sketch_stream(ids, w.astype(np.float64), k, 77)
+    assert rc == 0
+    assert_regs(y.cpu().numpy(), s.cpu().numpy().view(np.uint64), yo, so)
