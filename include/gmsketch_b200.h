@@ -123,6 +123,25 @@ int gm_sketch_elements(const void *ids, int id_bits, const void *w, int w_bits,
                        uint64_t stream_salt, uint32_t flags, double *y_io,
                        uint64_t *s_io, int64_t *emitted_out, void *stream);
 
+/*
+ * gm_sketch_elements without any host synchronisation, for a stream of
+ * sketches: enqueues one pass that walks every element whose first arrival
+ * is within the list bound tau_hi (R x the first threshold, K2),
+ * so the sketch is complete unless the sampled weight was off by more than
+ * that margin.  When the pass ends, the number of registers still unset is
+ * written to *unset_out (DEVICE int); if it is non-zero after the stream is
+ * synchronised, finish the sketch with gm_sketch_elements(...,
+ * GM_FLAG_ACCUMULATE) over the same elements (registers already set stay
+ * valid: an element's arrivals are folded idempotently).  Data errors are
+ * latched and returned by gm_stream_status().  n >= 1; GM_FLAG_EXHAUSTIVE is
+ * not accepted; GM_FLAG_ACCUMULATE is.
+ */
+int gm_sketch_elements_async(const void *ids, int id_bits, const void *w,
+                             int w_bits, int64_t n, int32_t k,
+                             uint64_t global_seed, uint64_t stream_salt,
+                             uint32_t flags, double *y_io, uint64_t *s_io,
+                             int32_t *unset_out, void *stream);
+
 /* Same contract with HOST buffers. */
 int gm_sketch_elements_host(const void *ids, int id_bits, const void *w,
                             int w_bits, int64_t n, int32_t k,

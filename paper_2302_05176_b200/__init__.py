@@ -62,6 +62,7 @@ from .sketch import (
     sketch_csr_host_many,
     exact_y_host,
     sketch_elements,
+    sketch_elements_many,
     sketch_fast,
     sketch_fast_counted,
     sketch_from_json,

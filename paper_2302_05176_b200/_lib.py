@@ -45,6 +45,7 @@ SIGNATURES = {
     "gm_sketch_csr_host": (_int, [_vp, _int, _vp, _int, _vp, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),
     "gm_sketch_elements": (_int, [_vp, _int, _vp, _int, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),
     "gm_sketch_elements_host": (_int, [_vp, _int, _vp, _int, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),
+    "gm_sketch_elements_async": (_int, [_vp, _int, _vp, _int, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),
     "gm_merge": (_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp]),
     "gm_match_count": (_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
     "gm_cardinality": (_int, [_vp, _i64, _i32, _vp, _vp, _vp]),

@@ -340,7 +340,10 @@ int check_common(int id_bits, int w_bits, int32_t k) {
 template <class IdT, class WT>
 int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u64 pseed,
                  uint32_t flags, double* y_io, u64* s_io, int64_t* emitted_out, Workspace* ws,
-                 cudaStream_t st) {
+                 cudaStream_t st, int* unset_async = nullptr) {
+  // unset_async != nullptr: one pass, walked at the list bound, enqueued
+  // without any host synchronisation; the unset-register count goes to
+  // *unset_async (device) when the pass ends (gm_sketch_elements_async)
   int rc = grow(&ws->regs, &ws->regs_cap, (size_t)k, st);
   if (rc) return rc;
   const unsigned rgrid = (k + 255) / 256;
@@ -370,7 +373,7 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
     static const double tau_scale = getenv("GM_ELEM_TAU_SCALE") ? atof(getenv("GM_ELEM_TAU_SCALE")) : 1.0;
     static const double r_fixed = getenv("GM_ELEM_R") ? atof(getenv("GM_ELEM_R")) : 0.0;
     TauArgs targs{ws->dbl, ws->sample_part, sgrid, k, (double)n / (double)std::max<int64_t>(sampled, 1),
-                  tau_scale, r_fixed, ws->ull};
+                  tau_scale, r_fixed, ws->ull, unset_async ? 1 : 0};
     weight_sample_kernel<IdT, WT><<<sgrid, 256, 0, st>>>((const IdT*)ids, (const WT*)w, n, ws->sample_set, tcap,
                                                          ws->sample_part, fold_init ? ws->regs : nullptr, k,
                                                          ws->counters + 1, targs, (unsigned*)(ws->counters + 3));
@@ -397,6 +400,19 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
     int surv_per_sm = 0;  // the list walk is latency-bound: as many resident CTAs as fit
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&surv_per_sm, elem_survivor_kernel, NT, 0));
     surv_per_sm = std::max(surv_per_sm, 1);
+    if (unset_async) {  // one pass at the list bound, nothing read back
+      elem_filter_kernel<IdT, WT><<<(unsigned)fgrid, NT, 0, st>>>(
+          (const IdT*)ids, (const WT*)w, n, k, useed, ws->dbl + 3, ws->surv, surv_cap, ws->ull + 2, nullptr, ws->err);
+      elem_survivor_kernel<<<(unsigned)(num_sms() * surv_per_sm), NT, 0, st>>>(
+          ws->surv, ws->ull + 2, surv_cap, k, useed, pseed, ws->dbl, ws->regs, ws->counters + 1, ws->heavy,
+          (int64_t)ws->heavy_cap, ws->ull, nullptr);
+      elem_heavy_kernel<IdT, WT><<<(unsigned)heavy_blocks, NT, 0, st>>>(
+          (const IdT*)ids, (const WT*)w, ws->surv, k, useed, pseed, ws->dbl, ws->regs, ws->counters + 1, ws->heavy,
+          ws->ull, (int64_t)ws->heavy_cap, ws->dense, nullptr, (unsigned*)(ws->counters + 2), y_io, s_io);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(unset_async, ws->counters + 1, sizeof(int), cudaMemcpyDeviceToDevice, st));
+      return GM_OK;
+    }
     const double lk = std::log((double)k);
     double tau_h = 0.0, tau_hi_h = 0.0, R = 2.0;
     bool list_ok = false;  // the survivor list holds every element with first arrival <= tau_hi_h
@@ -815,6 +831,31 @@ int gm_sketch_elements(const void* ids, int id_bits, const void* w, int w_bits, 
   if (unset > 0)
     return fail(GM_ERR_INCOMPLETE, "IncompleteSketchError: %d register(s) unset", unset);
   return GM_OK;
+}
+
+int gm_sketch_elements_async(const void* ids, int id_bits, const void* w, int w_bits, int64_t n,
+                             int32_t k, uint64_t global_seed, uint64_t stream_salt, uint32_t flags,
+                             double* y_io, uint64_t* s_io, int32_t* unset_out, void* stream) {
+  g_msg[0] = 0;
+  (void)cudaGetLastError();
+  int rc = check_common(id_bits, w_bits, k);
+  if (rc) return rc;
+  if (n < 1) return fail(GM_ERR_INVALID_PARAMETER, "gm_sketch_elements_async needs n >= 1");
+  if (!unset_out) return fail(GM_ERR_INVALID_PARAMETER, "unset_out must be a device int");
+  if (flags & GM_FLAG_EXHAUSTIVE) return fail(GM_ERR_INVALID_PARAMETER, "GM_FLAG_EXHAUSTIVE needs gm_sketch_elements");
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace* ws = nullptr;
+  rc = get_ws(st, &ws);
+  if (rc) return rc;
+  const u64 useed = global_seed, pseed = global_seed ^ stream_salt;
+  const u32 kk = (u32)k;
+  if (id_bits == 32 && w_bits == 32)
+    return run_elements<u32, float>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, nullptr, ws, st, unset_out);
+  if (id_bits == 32)
+    return run_elements<u32, double>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, nullptr, ws, st, unset_out);
+  if (w_bits == 32)
+    return run_elements<u64, float>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, nullptr, ws, st, unset_out);
+  return run_elements<u64, double>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, nullptr, ws, st, unset_out);
 }
 
 int gm_sketch_elements_host(const void* ids, int id_bits, const void* w, int w_bits, int64_t n,

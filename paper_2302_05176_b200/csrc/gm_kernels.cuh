@@ -537,6 +537,7 @@ struct TauArgs {
   double scale;             // n / sampled items
   double tau_scale, r_fixed;  // test knobs (1, 0 by default)
   unsigned long long* ctr4;   // cleared: heavy count, emitted, list count, spare
+  int walk_hi;                // walk the list at tau_hi whatever the duplication (one-pass calls)
 };
 
 // (one block of 256 threads; the partials are summed in a fixed order)
@@ -576,7 +577,7 @@ __device__ __forceinline__ void tau_block(const TauArgs& A) {
   // its first tau would come from an over-estimated W, and a failed walk costs
   // a host round trip and a second walk (the list walk is ~1 arrival per
   // listed element either way)
-  tau[0] = (ratio > 1.5 && A.r_fixed <= 0.0) ? tau[3] : t0;
+  tau[0] = ((ratio > 1.5 || A.walk_hi) && A.r_fixed <= 0.0) ? tau[3] : t0;
 }
 
 // Blocked sample of the stream: block b of the grid reads the contiguous

@@ -34,6 +34,7 @@ import torch
 from . import _device, _lib
 from .errors import (
     EmptyVectorError,
+    IncompleteSketchError,
     InvalidParameterError,
     InvalidWeightError,
     MismatchedSketchError,
@@ -411,6 +412,37 @@ def sketch_elements(ids, weights, k: int, scheme: SeedScheme, *, exhaustive: boo
                  _device.w_bits_of(w_t), ids_t.numel(), k, scheme.global_seed, scheme.stream_salt,
                  flags, y.data_ptr(), s.data_ptr(), em.ctypes.data, _device.stream_ptr())
     return y, s, int(em[0])
+
+
+def sketch_elements_many(sets, k: int, scheme: SeedScheme):
+    """One sketch per (ids, weights) element set, enqueued back to back on the
+    current stream without host synchronisation between them
+    (gm_sketch_elements_async: one pass at the list bound each); one
+    synchronisation at the end reads the unset-register counts, and a sketch
+    that needs it is finished with the synchronous call (GM_FLAG_ACCUMULATE).
+    Returns [(y [k] float64, s [k] int64 view of uint64)] in order, equal to
+    sketch_elements per set."""
+    _check_k(k)
+    dev = _device.require_cuda()
+    sets = [(ids if isinstance(ids, torch.Tensor) else torch.from_numpy(_as_id_np(ids)),
+             w if isinstance(w, torch.Tensor) else torch.from_numpy(_device.weight_array(w)[0])) for ids, w in sets]
+    sets = [(i.to(dev).contiguous(), w.to(dev).contiguous()) for i, w in sets]
+    out = [(torch.empty(k, dtype=torch.float64, device=dev), torch.empty(k, dtype=torch.int64, device=dev))
+           for _ in sets]
+    unset = torch.zeros(max(1, len(sets)), dtype=torch.int32, device=dev)
+    sp = _device.stream_ptr()
+    for j, ((i, w), (y, s)) in enumerate(zip(sets, out)):
+        if i.numel() == 0:
+            raise IncompleteSketchError([])
+        _device.call("gm_sketch_elements_async", i.data_ptr(), _device.id_bits_of(i), w.data_ptr(),
+                     _device.w_bits_of(w), i.numel(), k, scheme.global_seed, scheme.stream_salt, 0,
+                     y.data_ptr(), s.data_ptr(), unset[j].data_ptr(), sp)
+    counts = unset.cpu().numpy()  # the one synchronisation
+    _device.call("gm_stream_status", sp)
+    for j, ((i, w), (y, s)) in enumerate(zip(sets, out)):
+        if counts[j] > 0:
+            sketch_elements(i, w, k, scheme, into=(y, s))
+    return out
 
 
 def _to_sketch(k, y: np.ndarray, s: np.ndarray, fp: int) -> GumbelMaxSketch:

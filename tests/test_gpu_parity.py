@@ -737,3 +737,46 @@ def test_elements_small_sets_with_repeats(n, k):
     rc, yo, so, _, _ = O.sketch_stream(ids, w.astype(np.float64), k, 77)
     assert rc == 0
     assert_regs(y.cpu().numpy(), s.cpu().numpy().view(np.uint64), yo, so)
+
+
+_ASYNC_SCRIPT = r"""
+import sys, json
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2302_05176_b200 as gm
+from paper_2302_05176_b200 import workloads
+ids4, w4, k4, seed = workloads.config4(n_pairs=1_000_000, n_keys=10**6)
+rng = np.random.default_rng(9)
+w5 = rng.lognormal(0.0, 2.0, 2_000_000).astype(np.float32)
+ids5 = np.arange(w5.size, dtype=np.uint32)
+sets = [(ids4, w4), (ids5, w5), (ids4[:5000], w4[:5000]), (ids5[:300], w5[:300])]
+out = gm.sketch_elements_many(sets, 2048, gm.SeedScheme(seed))
+print(json.dumps([[y.cpu().numpy().tobytes().hex(), s.cpu().numpy().tobytes().hex()] for y, s in out]))
+"""
+
+
+@pytest.mark.parametrize("env", [{}, {"GM_ELEM_TAU_SCALE": "0.1"}])
+def test_elements_many_async_equals_sync(env):
+    """sketch_elements_many (gm_sketch_elements_async, one pass at the list
+    bound per set, no host sync between sets) equals the oracle per set; with
+    the first tau scaled down tenfold the one-pass sketches come back
+    incomplete and are finished by the synchronous accumulate call."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", _ASYNC_SCRIPT, root], capture_output=True, text=True,
+                         env={**os.environ, **env}, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    out = json.loads(res.stdout.strip().splitlines()[-1])
+    ids4, w4, k4, seed = workloads.config4(n_pairs=1_000_000, n_keys=10**6)
+    rng = np.random.default_rng(9)
+    w5 = rng.lognormal(0.0, 2.0, 2_000_000).astype(np.float32)
+    ids5 = np.arange(w5.size, dtype=np.uint64)
+    sets = [(ids4, w4), (ids5, w5), (ids4[:5000], w4[:5000]), (ids5[:300], w5[:300])]
+    for (i, w), (yh, sh) in zip(sets, out):
+        rc, yo, so, _, _ = O.sketch_stream(i, w.astype(np.float64), 2048, seed)
+        assert rc == 0
+        assert_regs(np.frombuffer(bytes.fromhex(yh), np.float64), np.frombuffer(bytes.fromhex(sh), np.uint64), yo, so)
