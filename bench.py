@@ -296,7 +296,7 @@ def run_ours_elements(args, rank, world, local_rank):
 
     def finish(steps):
         """read the unset counts (one sync); complete a sketch that needs it"""
-        if int((unset[:steps] > 0).sum().item()):
+        if (unset[:steps].cpu().numpy() > 0).any():  # a copy, no kernel
             redone[0] += 1
             rc = L.gm_sketch_elements(d_ids.data_ptr(), id_bits, d_w.data_ptr(), 32, n, k, scheme.global_seed,
                                       scheme.stream_salt, _lib.GM_FLAG_ACCUMULATE, y.data_ptr(), s.data_ptr(), 0, sp)
