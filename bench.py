@@ -58,6 +58,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5])
     p.add_argument("--n", type=float, default=0, help="configs 4/5: override the element count (default: BASELINE size)")
+    p.add_argument("--elem-streams", type=int, default=3, help="configs 4/5 at N=1: CUDA streams the sketches rotate over")
     p.add_argument("--merge", default="allgather", choices=["allgather", "allreduce"],
                    help="configs 4/5, N > 1: all-gather + rank-order device merge, or two MIN all-reduces")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -278,35 +279,50 @@ def run_ours_elements(args, rank, world, local_rank):
     # (gm_sketch_elements_async, no host synchronisation between sketches) and
     # writes its unset-register count to the device; after the K steps the
     # counts are read and any incomplete sketch is finished synchronously
-    # (GM_FLAG_ACCUMULATE) inside the timed region.
-    unset = torch.zeros(max(args.steps, args.warmup, 3), dtype=torch.int32, device=dev)
+    # (GM_FLAG_ACCUMULATE) inside the timed region.  At N = 1 the sketches
+    # rotate over --elem-streams CUDA streams (each with its own workspace), so
+    # one sketch's latency-bound list walk overlaps the next one's filter; at
+    # N > 1 one stream carries the sketches and the register exchanges.
+    ns_e = max(1, args.elem_streams) if world == 1 else 1
+    estreams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(ns_e - 1)]
+    outs = [(y, s)] + [(torch.empty_like(y), torch.empty_like(s)) for _ in range(ns_e - 1)]
+    n_warm = max(3, args.warmup, 2 * ns_e)  # every stream's workspace is created and grown before timing
+    unset = torch.zeros(max(args.steps, n_warm), dtype=torch.int32, device=dev)
     redone = [0]
 
     def step(i):
+        st_, (yy, ss_) = estreams[i % ns_e], outs[i % ns_e]
         rc = L.gm_sketch_elements_async(d_ids.data_ptr(), id_bits, d_w.data_ptr(), 32, n, k, scheme.global_seed,
-                                        scheme.stream_salt, 0, y.data_ptr(), s.data_ptr(),
-                                        unset[i].data_ptr(), sp)
+                                        scheme.stream_salt, 0, yy.data_ptr(), ss_.data_ptr(),
+                                        unset[i].data_ptr(), st_.cuda_stream)
         if rc:
             raise RuntimeError(_lib.last_error())
         if world > 1:
             if args.merge == "allreduce":
-                return shard.allreduce_min_registers(y, s)
-            return shard.merge_across_ranks(y, s)
-        return y, s
+                return shard.allreduce_min_registers(yy, ss_)
+            return shard.merge_across_ranks(yy, ss_)
+        return yy, ss_
 
     def finish(steps):
-        """read the unset counts (one sync); complete a sketch that needs it"""
-        if (unset[:steps].cpu().numpy() > 0).any():  # a copy, no kernel
+        """join the streams, read the unset counts; complete a sketch that needs it"""
+        for st_ in estreams[1:]:
+            e = torch.cuda.Event()
+            e.record(st_)
+            stream.wait_event(e)
+        cnt = unset[:steps].cpu().numpy()  # a copy, no kernel
+        for j in np.nonzero(cnt > 0)[0]:
             redone[0] += 1
+            yy, ss_ = outs[int(j) % ns_e]
             rc = L.gm_sketch_elements(d_ids.data_ptr(), id_bits, d_w.data_ptr(), 32, n, k, scheme.global_seed,
-                                      scheme.stream_salt, _lib.GM_FLAG_ACCUMULATE, y.data_ptr(), s.data_ptr(), 0, sp)
+                                      scheme.stream_salt, _lib.GM_FLAG_ACCUMULATE, yy.data_ptr(), ss_.data_ptr(), 0, sp)
             if rc:
                 raise RuntimeError(_lib.last_error())
-        _device.call("gm_stream_status", sp)
+        for st_ in estreams:
+            _device.call("gm_stream_status", st_.cuda_stream)
 
-    for i in range(max(3, args.warmup)):
+    for i in range(n_warm):
         step(i)
-    finish(max(3, args.warmup))
+    finish(n_warm)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -314,6 +330,8 @@ def run_ours_elements(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clocks:
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(stream)
+        for st_ in estreams[1:]:
+            st_.wait_event(a0)
         for i in range(args.steps):
             yo, so = step(i)
         finish(args.steps)
@@ -393,7 +411,8 @@ def run_ours_elements(args, rank, world, local_rank):
                    "parallelism": (f"element shards x{world} + NCCL " + ("MIN all-reduces" if args.merge == "allreduce"
                                    else "all-gather + device merge")) if world > 1 else "single GPU",
                    "l2": f"inputs ({(ids.nbytes + w.nbytes) >> 20} MiB) larger than the 126 MB L2",
-                   "schedule": "a stream of one-pass sketches (gm_sketch_elements_async, no host sync between them); "
+                   "schedule": f"a stream of one-pass sketches over {ns_e} CUDA stream(s) (gm_sketch_elements_async, "
+                               "no host sync between them); "
                                f"incomplete ones finished synchronously in the timed region ({redone[0]} needed it)"},
         "e2e": {"value": n_all / (e2e_ms / 1e3), "unit": "elements/s", "h2d_bytes_per_step": in_bytes,
                 "d2h_bytes_per_step": 16 * k, "ms_per_step": e2e_ms,
