@@ -348,6 +348,20 @@ def run_ours_elements(args, rank, world, local_rank):
     step_ms = total_ms / args.steps
     value = n_all / (step_ms / 1e3)
 
+    # one sketch alone through the synchronous call (its latency, reported beside the stream figure)
+    lat = []
+    for _ in range(5):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        rc = L.gm_sketch_elements(d_ids.data_ptr(), id_bits, d_w.data_ptr(), 32, n, k, scheme.global_seed,
+                                  scheme.stream_salt, 0, y.data_ptr(), s.data_ptr(), 0, sp)
+        if rc:
+            raise RuntimeError(_lib.last_error())
+        a1.record(stream)
+        torch.cuda.synchronize()
+        lat.append(a0.elapsed_time(a1))
+    sketch_ms = statistics.median(lat)
+
     # end to end: host buffers through gm_sketch_elements_host (every step copies
     # the shard in and the k registers out), merged across ranks on the host side
     h_ids = torch.from_numpy(h_ids_np.view(np.int64 if id_bits == 64 else np.int32)).pin_memory()
@@ -413,7 +427,9 @@ def run_ours_elements(args, rank, world, local_rank):
                    "l2": f"inputs ({(ids.nbytes + w.nbytes) >> 20} MiB) larger than the 126 MB L2",
                    "schedule": f"a stream of one-pass sketches over {ns_e} CUDA stream(s) (gm_sketch_elements_async, "
                                "no host sync between them); "
-                               f"incomplete ones finished synchronously in the timed region ({redone[0]} needed it)"},
+                               f"incomplete ones finished synchronously in the timed region ({redone[0]} needed it)",
+                   "sketch_latency_ms": sketch_ms,
+                   "sketch_latency_note": "one sketch alone through the synchronous gm_sketch_elements (median of 5)"},
         "e2e": {"value": n_all / (e2e_ms / 1e3), "unit": "elements/s", "h2d_bytes_per_step": in_bytes,
                 "d2h_bytes_per_step": 16 * k, "ms_per_step": e2e_ms,
                 "api": "gm_sketch_elements_host (pinned host buffers), wall clock"},
