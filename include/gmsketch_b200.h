@@ -55,7 +55,7 @@ extern "C" {
 #define GM_FLAG_ASYNC 0x1u       /* enqueue only; see gm_stream_status()           */
 #define GM_FLAG_EXHAUSTIVE 0x2u  /* run every queue to k (sketch_naive semantics)  */
 #define GM_FLAG_ACCUMULATE 0x4u  /* gm_sketch_elements: fold into y_io/s_io        */
-#define GM_FLAG_SPLIT 0x8u       /* gm_sketch_csr: experimental split schedule     */
+/* 0x8u: reserved (was an experimental split schedule, removed) */
 #define GM_FLAG_S32 0x10u        /* gm_sketch_csr_host: s_out is uint32 (32-bit ids) */
 
 /* Library version (major*10000 + minor*100 + patch). */
@@ -68,6 +68,18 @@ const char *gm_last_error(void);
 /* Returns and clears the data error latched on `stream` by GM_FLAG_ASYNC
  * calls; synchronises the stream. */
 int gm_stream_status(void *stream);
+
+/* Lifecycle.  Scratch (device buffers, a page-locked readback word block)
+ * is created lazily per (device, stream) by the first call on a stream and
+ * reused by later calls on it.  gm_release_stream synchronises `stream` and
+ * frees its scratch (call it before destroying a stream the library has
+ * used); gm_finalize synchronises every device used and frees all scratch.
+ * The library never retains caller memory.  gm_workspace_count: live
+ * (device, stream) scratch sets.  (The reference is pure functions with no
+ * retained state; this is the B200 engine's own housekeeping.) */
+int gm_release_stream(void *stream);
+int gm_finalize(void);
+int gm_workspace_count(void);
 
 /*
  * Batch of independent CSR vectors -> n_vec sketches.
@@ -182,6 +194,13 @@ int gm_uniform_open_batch(const uint64_t *global_seeds, const uint64_t *elements
 int gm_perm_draw_batch(const uint64_t *perm_seeds, const uint64_t *elements,
                        const uint64_t *steps, const uint32_t *ks, int64_t n,
                        uint32_t *out, void *stream);
+/* rand_int_between(scheme, e, step, lo, hi) over ANY range (randgen.py:122-143):
+ * out[i] = (result - lo), the offset in [0, m), m = m_minus_1[i] + 1 <= 2^64
+ * (m_minus_1 = UINT64_MAX means m = 2^64); keys (perm_seeds[i], elements[i]
+ * mod 2^64, steps[i] mod 2^64).  (device) arrays; synchronises. */
+int gm_rand_int_between_batch(const uint64_t *perm_seeds, const uint64_t *elements,
+                              const uint64_t *steps, const uint64_t *m_minus_1,
+                              int64_t n, uint64_t *out, void *stream);
 
 /* Arithmetic self-checks (device).
  * gm_arith_check: over n keyed random inputs, counts[0] = #(branch-free

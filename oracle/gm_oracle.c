@@ -47,6 +47,17 @@ double gmo_uniform_open(uint64_t global_seed, uint64_t element, uint64_t step) {
   return u_from_bits(gmo_mix64(global_seed + element * K_ELEM + step * K_STEP));
 }
 
+/* The keyed uniforms u_i = uniform_open(seed, i0 + i, 1) and glibc's
+ * log(u_i) (what math.log returns, randgen.py:186): the checker of the
+ * device log. */
+void gmo_log_uniforms(uint64_t seed, int64_t i0, int64_t n, double *u_out, double *log_out) {
+  for (int64_t i = 0; i < n; ++i) {
+    const double u = gmo_uniform_open(seed, (uint64_t)(i0 + i), 1);
+    u_out[i] = u;
+    log_out[i] = log(u);
+  }
+}
+
 /* 2**64 mod m, for m >= 1 */
 static inline uint64_t pow64_mod(uint64_t m) { return (UINT64_MAX % m + 1) % m; }
 

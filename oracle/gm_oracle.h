@@ -79,6 +79,8 @@ int gmo_sketch_csr(const uint64_t *ids, const double *w,
                    int threads, double *y, uint64_t *s, int64_t *emitted);
 /* estimate.py:103-125: per register strict '<', earlier sketch wins ties.
  * y_in/s_in are n_sk*k row-major. */
+/* uniform_open(seed, i0 + i, 1) and glibc log of it, i < n */
+void gmo_log_uniforms(uint64_t seed, int64_t i0, int64_t n, double *u_out, double *log_out);
 void gmo_merge(const double *y_in, const uint64_t *s_in, int64_t n_sk,
                int32_t k, double *y_out, uint64_t *s_out);
 

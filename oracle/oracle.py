@@ -59,6 +59,8 @@ def lib():
         L.gmo_sketch_stream.argtypes = [vp, vp, i64, i32, u64, u64, ctypes.c_int, vp, vp, vp, vp]
         L.gmo_sketch_csr.restype = ctypes.c_int
         L.gmo_sketch_csr.argtypes = [vp, vp, vp, i64, i32, u64, u64, ctypes.c_int, ctypes.c_int, vp, vp, vp]
+        L.gmo_log_uniforms.restype = None
+        L.gmo_log_uniforms.argtypes = [u64, i64, i64, vp, vp]
         L.gmo_merge.restype = None
         L.gmo_merge.argtypes = [vp, vp, i64, i32, vp, vp]
         _lib = L
@@ -175,3 +177,12 @@ def merge(y, s):
     so = np.empty(k, np.uint64)
     lib().gmo_merge(_p(y), _p(s), n, k, _p(yo), _p(so))
     return yo, so
+
+
+def log_uniforms(seed: int, i0: int, n: int):
+    """(u, log u) for the keyed uniforms uniform_open(seed, i0 + i, 1),
+    i < n, with glibc's log (math.log; randgen.py:107-119, :186)."""
+    u = np.empty(n, np.float64)
+    lg = np.empty(n, np.float64)
+    lib().gmo_log_uniforms(seed & MASK64, i0, n, _p(u), _p(lg))
+    return u, lg

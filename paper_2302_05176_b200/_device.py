@@ -27,6 +27,21 @@ def stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+_POOLS: dict[tuple[int, int], list] = {}
+
+
+def stream_pool(dev: torch.device, n: int) -> list:
+    """n CUDA streams of `dev`, created once per process and reused: the
+    library keeps scratch per (device, stream), so fresh streams per call
+    would each leave a workspace behind (gm_release_stream frees one)."""
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), n)
+    pool = _POOLS.get(key)
+    if pool is None:
+        pool = [torch.cuda.Stream(device=dev) for _ in range(n)]
+        _POOLS[key] = pool
+    return pool
+
+
 def call(name: str, *args) -> int:
     rc = getattr(_lib.load(), name)(*args)
     if rc:

@@ -27,7 +27,6 @@ GM_ERR_NO_DEVICE = 101
 GM_FLAG_ASYNC = 0x1
 GM_FLAG_EXHAUSTIVE = 0x2
 GM_FLAG_ACCUMULATE = 0x4
-GM_FLAG_SPLIT = 0x8
 GM_FLAG_S32 = 0x10
 
 # every symbol include/gmsketch_b200.h declares: (name, restype, argtypes)
@@ -41,6 +40,9 @@ SIGNATURES = {
     "gm_stats_read": (_int, [_vp]),
     "gm_trace_read": (_int, [_vp, _vp]),
     "gm_stream_status": (_int, [_vp]),
+    "gm_release_stream": (_int, [_vp]),
+    "gm_finalize": (_int, []),
+    "gm_workspace_count": (_int, []),
     "gm_sketch_csr": (_int, [_vp, _int, _vp, _int, _vp, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),
     "gm_sketch_csr_host": (_int, [_vp, _int, _vp, _int, _vp, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),
     "gm_sketch_elements": (_int, [_vp, _int, _vp, _int, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),
@@ -51,6 +53,7 @@ SIGNATURES = {
     "gm_cardinality": (_int, [_vp, _i64, _i32, _vp, _vp, _vp]),
     "gm_uniform_open_batch": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "gm_perm_draw_batch": (_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "gm_rand_int_between_batch": (_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "gm_arith_check": (_int, [_i64, _u64, _vp, _vp]),
     "gm_log_batch": (_int, [_vp, _i64, _vp, _vp]),
     "gm_check_pairs": (_int, [_vp, _int, _vp, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -13,11 +13,11 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <utility>
 
 #include "../../include/gmsketch_b200.h"
 #include "gm_csr.cuh"
-#include "gm_split.cuh"
 #include "gm_pairs.cuh"
 
 #include <cub/device/device_scan.cuh>
@@ -57,30 +57,6 @@ struct Workspace {
   size_t heavy_cap = 0;
   u32* dense = nullptr;
   size_t dense_cap = 0;
-  u32* resume = nullptr;
-  size_t resume_cap = 0;
-  // split CSR path
-  u32* sp_vec = nullptr;                   // element -> vector
-  size_t sp_vec_cap = 0;
-  u32* sp_depth = nullptr;                 // accepted arrivals per element
-  size_t sp_depth_cap = 0;
-  unsigned long long* sp_aoff = nullptr;   // exclusive scan of depth
-  size_t sp_aoff_cap = 0;
-  void* sp_scan_tmp = nullptr;
-  size_t sp_scan_cap = 0;
-  double* sp_t = nullptr;                  // arrival times
-  size_t sp_t_cap = 0;
-  unsigned short* sp_j = nullptr;          // draws j - 1
-  size_t sp_j_cap = 0;
-  u32* sp_e = nullptr;                     // element of each arrival
-  size_t sp_e_cap = 0;
-  Reg* sp_regs = nullptr;                  // registers of the batch
-  size_t sp_regs_cap = 0;
-  u32* sp_dense = nullptr;                 // fy_kernel carry arrays
-  size_t sp_dense_cap = 0;
-  int* sp_redo = nullptr;                  // vectors to re-run
-  size_t sp_redo_cap = 0;
-  unsigned long long* sp_ctr = nullptr;    // [0..2] feeders, [3] n_redo (int), [4] total arrivals
   u32* csr_dense = nullptr;                // CSR warp-walker dense arrays (stamped)
   size_t csr_dense_cap = 0;
   double* vsum = nullptr;                  // per-vector total weight (CSR prep)
@@ -103,6 +79,17 @@ struct Workspace {
 
 std::mutex g_mu;
 std::map<std::pair<int, cudaStream_t>, Workspace*> g_ws;
+
+// Frees a workspace (the caller has synchronised its stream).
+void free_ws(Workspace* w) {
+  void* dev_ptrs[] = {w->counters, w->err, w->ull, w->dbl, w->regs, w->heavy, w->dense, w->csr_dense,
+                      w->vsum, w->vflag, w->surv, w->sample_set, w->sample_part, w->stage, w->pt_keys,
+                      w->pt_first};
+  for (void* p : dev_ptrs)
+    if (p) cudaFree(p);
+  if (w->host) cudaFreeHost(w->host);
+  delete w;
+}
 
 int get_ws(cudaStream_t st, Workspace** out) {
   int dev = 0;
@@ -131,14 +118,18 @@ int get_ws(cudaStream_t st, Workspace** out) {
   return GM_OK;
 }
 
+// Grow a stream-ordered scratch buffer.  The new buffer is allocated before
+// the old one is freed, so a failed allocation leaves (*p, *cap) valid.
 template <class T>
 int grow(T** p, size_t* cap, size_t need, cudaStream_t st, bool zero = false) {
   if (*cap >= need) return GM_OK;
-  if (*p) CK(cudaFreeAsync(*p, st));
   size_t n = need + need / 4;
-  CK(cudaMallocAsync((void**)p, n * sizeof(T), st));
-  if (zero) CK(cudaMemsetAsync(*p, 0, n * sizeof(T), st));
+  T* q = nullptr;
+  CK(cudaMallocAsync((void**)&q, n * sizeof(T), st));
+  if (*p) CK(cudaFreeAsync(*p, st));
+  *p = q;
   *cap = n;
+  if (zero) CK(cudaMemsetAsync(*p, 0, n * sizeof(T), st));
   return GM_OK;
 }
 
@@ -173,35 +164,17 @@ int check_sync(Workspace* ws, cudaStream_t st, unsigned long long vec_base = 0) 
 }
 
 int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return sms;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
 }
 
 using CsrDefault = CsrCfg<256, 16, 2, 2, 75, 4>;
-// alternates for tuning sweeps (GM_CSR_CFG=1..3 selects one for u32 ids + f32 weights;
-// 1 = without the drain hand-over)
-using CsrAlt1 = CsrCfg<256, 16, 2, 2, 75, 0>;
-using CsrAlt2 = CsrCfg<256, 16, 2, 2, 85, 4>;
-using CsrAlt3 = CsrCfg<256, 16, 2, 2, 95, 4>;
 // k <= 512: four vector slots fit in the shared memory two slots of k = 1024
 // take, so a CTA keeps four (small) vectors in flight -- fewer lanes idle
 // while a slot drains (config 3: 19.4 -> 16.4 ms per batch)
 using CsrSmallK = CsrCfg<256, 16, 4, 2, 75, 4>;
-using CsrAlt5 = CsrCfg<256, 16, 3, 2, 75, 4>;  // 3 vector slots
-
-int csr_cfg_choice() {
-  static int c = -1;
-  if (c < 0) {
-    const char* e = getenv("GM_CSR_CFG");
-    c = e ? atoi(e) : 0;
-  }
-  return c;
-}
 
 template <class C, class IdT, class WT>
 int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k,
@@ -213,14 +186,16 @@ int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n
   {
     // occupancy per (kernel, smem) is cached: the launch path stays a
     // memset + two kernel launches
+    // (per device: cudaFuncSetAttribute applies to the current device only)
     static std::mutex mu;
-    static std::map<std::pair<const void*, size_t>, int> cache;
+    static std::map<std::tuple<int, const void*, size_t>, int> cache;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_pair((const void*)kern, smem);
+    auto key = std::make_tuple(dev, (const void*)kern, smem);
     auto it = cache.find(key);
     if (it == cache.end()) {
-      int dev = 0, optin = 0;
-      CK(cudaGetDevice(&dev));
+      int optin = 0;
       CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
       cudaFuncAttributes fa;
       CK(cudaFuncGetAttributes(&fa, kern));
@@ -262,70 +237,6 @@ int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n
                                             inkernel ? nullptr : ws->vsum, inkernel ? nullptr : ws->vflag, y, s, em,
                                             ws->counters, ws->csr_dense, ws->err, attempt0, vec_list);
   CK(cudaGetLastError());
-  return GM_OK;
-}
-
-// Split CSR path (gm_split.cuh): depth pass, scan, arrival pass, Fisher-Yates
-// pass, finalize; vectors whose pass left a register unset are re-run with a
-// larger tau through the fused kernel.  Two host syncs (element count and
-// re-run count).
-template <class IdT, class WT>
-int launch_split(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k, u64 useed,
-                 u64 pseed, double* y, u64* s, int64_t* em, Workspace* ws, cudaStream_t st, int attempt0) {
-  int64_t n = 0;
-  CK(cudaMemcpyAsync(&n, offsets + n_vec, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  int rc;
-  if ((rc = grow(&ws->sp_vec, &ws->sp_vec_cap, (size_t)n + 1, st))) return rc;
-  if ((rc = grow(&ws->sp_depth, &ws->sp_depth_cap, (size_t)n + 1, st))) return rc;
-  if ((rc = grow(&ws->sp_aoff, &ws->sp_aoff_cap, (size_t)n + 1, st))) return rc;
-  if ((rc = grow(&ws->sp_regs, &ws->sp_regs_cap, (size_t)n_vec * k, st))) return rc;
-  if ((rc = grow(&ws->vsum, &ws->vsum_cap, (size_t)n_vec, st))) return rc;
-  if ((rc = grow(&ws->vflag, &ws->vflag_cap, (size_t)n_vec, st))) return rc;
-  if ((rc = grow(&ws->sp_redo, &ws->sp_redo_cap, (size_t)n_vec, st))) return rc;
-  if (!ws->sp_ctr) CK(cudaMalloc(&ws->sp_ctr, 8 * sizeof(unsigned long long)));
-  const int sms = num_sms();
-  const int64_t grid_v = std::min<int64_t>((n_vec + 7) / 8, (int64_t)sms * 16);
-  csr_prep_kernel<WT><<<(unsigned)grid_v, 256, 0, st>>>((const WT*)w, offsets, n_vec, ws->vsum, ws->vflag, ws->err);
-  vec_of_kernel<<<(unsigned)grid_v, 256, 0, st>>>(offsets, n_vec, ws->sp_vec);
-  regs_init_kernel<<<sms * 8, 256, 0, st>>>(ws->sp_regs, n_vec * (int64_t)k);
-  CK(cudaMemsetAsync(ws->sp_ctr, 0, 8 * sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(ws->sp_depth + n, 0, sizeof(u32), st));
-  const unsigned grid_a = (unsigned)(sms * 8);
-  arrivals_kernel<IdT, WT, false><<<grid_a, SPLIT_NT, 0, st>>>(
-      (const IdT*)ids, (const WT*)w, n, ws->sp_vec, ws->vsum, ws->vflag, k, useed, pseed, attempt0, ws->sp_depth,
-      nullptr, 0, nullptr, nullptr, nullptr, ws->sp_ctr + 0);
-  CK(cudaGetLastError());
-  size_t tmp = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ws->sp_depth, ws->sp_aoff, (int64_t)n + 1, st));
-  if ((rc = grow((unsigned char**)&ws->sp_scan_tmp, &ws->sp_scan_cap, tmp, st))) return rc;
-  CK(cub::DeviceScan::ExclusiveSum(ws->sp_scan_tmp, tmp, ws->sp_depth, ws->sp_aoff, (int64_t)n + 1, st));
-  unsigned long long total = 0;
-  CK(cudaMemcpyAsync(&total, ws->sp_aoff + n, sizeof(total), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if ((rc = grow(&ws->sp_t, &ws->sp_t_cap, (size_t)total + 1, st))) return rc;
-  if ((rc = grow(&ws->sp_j, &ws->sp_j_cap, (size_t)total + 1, st))) return rc;
-  if ((rc = grow(&ws->sp_e, &ws->sp_e_cap, (size_t)total + 1, st))) return rc;
-  arrivals_kernel<IdT, WT, true><<<grid_a, SPLIT_NT, 0, st>>>(
-      (const IdT*)ids, (const WT*)w, n, ws->sp_vec, ws->vsum, ws->vflag, k, useed, pseed, attempt0, ws->sp_depth,
-      ws->sp_aoff, (unsigned long long)ws->sp_t_cap, ws->sp_t, ws->sp_j, ws->sp_e, ws->sp_ctr + 1);
-  CK(cudaGetLastError());
-  const unsigned grid_b = (unsigned)(sms * 8);
-  if ((rc = grow(&ws->sp_dense, &ws->sp_dense_cap, (size_t)grid_b * (SPLIT_NT / 32) * k, st))) return rc;
-  fy_kernel<IdT><<<grid_b, SPLIT_NT, 0, st>>>((const IdT*)ids, n, ws->sp_vec, ws->sp_aoff, ws->sp_t, ws->sp_j,
-                                              ws->sp_e, k, ws->sp_regs, ws->sp_dense, ws->sp_ctr + 2);
-  CK(cudaGetLastError());
-  finalize_kernel<<<(unsigned)grid_v, 256, 0, st>>>(ws->sp_regs, n_vec, k, y, s, ws->sp_redo, (int*)(ws->sp_ctr + 3));
-  if (em) split_emitted_kernel<<<(unsigned)grid_v, 256, 0, st>>>(offsets, n_vec, ws->sp_depth, k, em);
-  CK(cudaGetLastError());
-  int n_redo = 0;
-  CK(cudaMemcpyAsync(&n_redo, ws->sp_ctr + 3, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (n_redo > 0) {  // a larger tau for those vectors, fused kernel (weights already validated)
-    rc = launch_csr<CsrDefault, IdT, WT>(ids, w, offsets, n_redo, k, useed, pseed, y, s, em, ws, st,
-                                          attempt0 + 1, ws->sp_redo, true);
-    if (rc) return rc;
-  }
   return GM_OK;
 }
 
@@ -467,6 +378,12 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
         // (its last CTA stores the registers: with every attempt, a no-op
         // rewrite when another follows, so a single-attempt call synchronises once)
         CK(cudaGetLastError());
+        // accumulate: a loaded register above this pass's tau is not final
+        // (counting only unset ones lost arrivals in (tau, y_old))
+        if (flags & GM_FLAG_ACCUMULATE) {
+          count_unfinished_kernel<<<1, 1024, 0, st>>>(ws->regs, k, ws->dbl, ws->counters + 1);
+          CK(cudaGetLastError());
+        }
         CK(cudaMemcpyAsync(ws->host, ws->counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(ws->host + 1, ws->ull, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(ws->host + 3, ws->ull + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -613,6 +530,49 @@ int gm_trace_read(unsigned long long* ev_out, unsigned* n_out) {
 #endif
 }
 
+// Lifecycle: scratch is created lazily per (device, stream) by the first
+// call on that stream and kept for the stream's next calls.
+int gm_release_stream(void* stream) {
+  g_msg[0] = 0;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  Workspace* w = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_ws.find(std::make_pair(dev, (cudaStream_t)stream));
+    if (it == g_ws.end()) return GM_OK;
+    w = it->second;
+    g_ws.erase(it);
+  }
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  free_ws(w);
+  CK(cudaGetLastError());
+  return GM_OK;
+}
+
+int gm_finalize(void) {
+  g_msg[0] = 0;
+  std::map<std::pair<int, cudaStream_t>, Workspace*> all;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    all.swap(g_ws);
+  }
+  int cur = 0;
+  CK(cudaGetDevice(&cur));
+  for (auto& kv : all) {
+    CK(cudaSetDevice(kv.first.first));
+    CK(cudaDeviceSynchronize());
+    free_ws(kv.second);
+  }
+  CK(cudaSetDevice(cur));
+  return GM_OK;
+}
+
+int gm_workspace_count(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return (int)g_ws.size();
+}
+
 int gm_stream_status(void* stream) {
   Workspace* ws = nullptr;
   int rc = get_ws((cudaStream_t)stream, &ws);
@@ -679,26 +639,9 @@ int gm_sketch_csr(const void* ids, int id_bits, const void* w, int w_bits, const
   const bool small_k = kk <= 512;  // CsrSmallK: four vector slots
   // exhaustive = a single pass with tau = +inf (pass_tau's last attempt)
   const int a0 = (flags & GM_FLAG_EXHAUSTIVE) ? 3 : 0;
-  if ((flags & GM_FLAG_SPLIT) && !(flags & GM_FLAG_EXHAUSTIVE)) {
-    if (id_bits == 32 && w_bits == 32)
-      rc = launch_split<u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
-    else if (id_bits == 32)
-      rc = launch_split<u32, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
-    else if (w_bits == 32)
-      rc = launch_split<u64, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
-    else
-      rc = launch_split<u64, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
-  } else if (id_bits == 32 && w_bits == 32)
-    switch (csr_cfg_choice()) {
-      case 4: rc = launch_csr<CsrDefault, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0); break;
-      case 1: rc = launch_csr<CsrAlt1, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0); break;
-      case 2: rc = launch_csr<CsrAlt2, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0); break;
-      case 3: rc = launch_csr<CsrAlt3, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0); break;
-      case 5: rc = launch_csr<CsrAlt5, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0); break;
-      default:
-        rc = small_k ? launch_csr<CsrSmallK, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0)
-                     : launch_csr<CsrDefault, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
-    }
+  if (id_bits == 32 && w_bits == 32)
+    rc = small_k ? launch_csr<CsrSmallK, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0)
+                 : launch_csr<CsrDefault, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
   else if (id_bits == 32)
     rc = small_k ? launch_csr<CsrSmallK, u32, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0)
                  : launch_csr<CsrDefault, u32, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
@@ -842,7 +785,8 @@ int gm_sketch_elements_async(const void* ids, int id_bits, const void* w, int w_
   if (rc) return rc;
   if (n < 1) return fail(GM_ERR_INVALID_PARAMETER, "gm_sketch_elements_async needs n >= 1");
   if (!unset_out) return fail(GM_ERR_INVALID_PARAMETER, "unset_out must be a device int");
-  if (flags & GM_FLAG_EXHAUSTIVE) return fail(GM_ERR_INVALID_PARAMETER, "GM_FLAG_EXHAUSTIVE needs gm_sketch_elements");
+  if (flags & (GM_FLAG_EXHAUSTIVE | GM_FLAG_ACCUMULATE))
+    return fail(GM_ERR_INVALID_PARAMETER, "GM_FLAG_EXHAUSTIVE / GM_FLAG_ACCUMULATE need gm_sketch_elements");
   cudaStream_t st = (cudaStream_t)stream;
   Workspace* ws = nullptr;
   rc = get_ws(st, &ws);
@@ -947,6 +891,18 @@ int gm_perm_draw_batch(const uint64_t* perm_seeds, const uint64_t* elements, con
   (void)cudaGetLastError();
   if (n <= 0) return GM_OK;
   randint_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(perm_seeds, elements, steps, ks, n, out);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return GM_OK;
+}
+
+int gm_rand_int_between_batch(const uint64_t* perm_seeds, const uint64_t* elements, const uint64_t* steps,
+                              const uint64_t* m_minus_1, int64_t n, uint64_t* out, void* stream) {
+  g_msg[0] = 0;
+  (void)cudaGetLastError();
+  if (n <= 0) return GM_OK;
+  randint_general_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(perm_seeds, elements, steps,
+                                                                                      m_minus_1, n, out);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   return GM_OK;

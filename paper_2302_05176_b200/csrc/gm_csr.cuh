@@ -85,7 +85,7 @@ __host__ __device__ constexpr size_t csr3_smem_bytes(u32 k) {
   return (size_t)C::V * k * sizeof(Reg)               // registers of the slots
          + (size_t)C::NT * C::SLOTS * 4              // lane tables
          + (size_t)C::MTAB * 4                       // Barrett table
-         + 128 * 32                                  // log table copy
+         + 128 * 16                                  // log table copy
          + (size_t)C::NWARP * 32 * (8 + 4)           // warp-walker scan + prov
          + (size_t)C::MTAB * 8;                      // 64-bit Barrett table
 }
@@ -159,7 +159,7 @@ struct Lane {
 // for a warp to resume).
 template <class C>
 __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const u64* mtab64, u32 k,
-                                         const double (*ltab)[4]) {
+                                         const double* ltab) {
   const bool acc = !fresh;
   const u32 zs = L.z + 1;
   // permutation draw of step zs and both first-bucket probes
@@ -185,7 +185,7 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
   // next arrival's spacing (independent of this step's permutation work)
   const u32 zn = acc ? min(zs + 1, k) : 1u;
   const u64 x = mix64(L.ubase + (u64)zn * K_STEP);
-  const double Lg = -log_pos_t<true>(u_open(x), ltab);
+  const double Lg = -log_pos_t(u_open(x), ltab);
   const double D = __dmul_rn(L.w, (double)(k - zn + 1));
   double dq = ddiv_fast(Lg, D);
   // fast case: no draw rejection, zi resolved in its first bucket, ji found
@@ -409,12 +409,11 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 
   u32* tables = reinterpret_cast<u32*>(smem_raw + (size_t)V * k * sizeof(Reg));
   u32* mtab = tables + (size_t)NT * C::SLOTS;
-  double (*ltab)[4] = reinterpret_cast<double (*)[4]>(mtab + C::MTAB);  // 16-byte aligned: MTAB*4 % 16 == 0
-  double* scan = reinterpret_cast<double*>(ltab + 128) + warp * 32;
-  int* prov = reinterpret_cast<int*>(reinterpret_cast<double*>(ltab + 128) + NWARP * 32) + warp * 32;
+  double* ltab = reinterpret_cast<double*>(mtab + C::MTAB);  // 128 x {invc, logc}; 16-byte aligned: MTAB*4 % 16 == 0
+  double* scan = ltab + 256 + warp * 32;
+  int* prov = reinterpret_cast<int*>(ltab + 256 + NWARP * 32) + warp * 32;
   // floor(2^64 / m) for m = k - z + 1, z < MTAB: the lane step's draw in one 64-bit Barrett reduction
-  u64* mtab64 = reinterpret_cast<u64*>(reinterpret_cast<int*>(reinterpret_cast<double*>(ltab + 128) + NWARP * 32) +
-                                       NWARP * 32);
+  u64* mtab64 = reinterpret_cast<u64*>(reinterpret_cast<int*>(ltab + 256 + NWARP * 32) + NWARP * 32);
   u32* mytab = tables + tid * 4;
   u32* dense = dense_global + ((size_t)blockIdx.x * NWARP + warp) * k;
 
@@ -422,7 +421,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     mtab[z] = (z >= 1 && z <= k) ? barrett_magic(k - z + 1) : 0u;
     mtab64[z] = (z >= 1 && z <= k) ? barrett_magic64(k - z + 1) : 0ull;
   }
-  for (u32 i = tid; i < 128 * 4; i += NT) ltab[i >> 2][i & 3] = gm_logtab[i >> 2][i & 3];
+  for (u32 i = tid; i < 256; i += NT) ltab[i] = gm_glog_tab[i >> 1][i & 1];
   tab_clear<C>(mytab);
   for (u32 i = lane; i < k; i += 32) dense[i] = 0;  // stamps restart every launch
   if (tid < V) {

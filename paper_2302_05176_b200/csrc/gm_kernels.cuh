@@ -512,6 +512,30 @@ __global__ void load_regs_kernel(Reg* regs, u32 k, const double* y, const u64* s
   }
 }
 
+// GM_FLAG_ACCUMULATE: after a pass at tau, the registers that are not yet
+// final -- unset, or above tau (an arrival of the new elements in (tau, y_j)
+// could still lower y_j; registers loaded from an earlier sketch are set but
+// not bounded by this pass's tau).  Overwrites the counter the walkers
+// decrement; one block.
+__global__ void __launch_bounds__(1024) count_unfinished_kernel(const Reg* regs, u32 k, const double* tau_p,
+                                                                int* out) {
+  const double tau = *tau_p;
+  int c = 0;
+  for (u32 j = threadIdx.x; j < k; j += blockDim.x) {
+    const u64 y = __ldcg(&regs[j].y);
+    c += (y == INF_BITS || __longlong_as_double((long long)y) > tau) ? 1 : 0;
+  }
+  c = __reduce_add_sync(0xFFFFFFFFu, c);
+  __shared__ int part[32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += part[i];
+    *out = t;
+  }
+}
+
 __global__ void store_regs_kernel(const Reg* regs, u32 k, double* y, u64* s) {
   for (u32 j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
     y[j] = __longlong_as_double((long long)regs[j].y);
@@ -820,6 +844,28 @@ __global__ void randint_kernel(const u64* pseeds, const u64* elems, const u64* s
                                const u32* ks, int64_t n, u32* out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = perm_draw(pseeds[i] + elems[i] * K_ELEM, (u32)steps[i], ks[i]);
+}
+
+// rand_int_between over any range m <= 2^64 (randgen.py:122-143): offset
+// x mod m of the first accepted rehash x of the (element, step) key, with the
+// reference's rejection bound 2^64 - (2^64 mod m).  m_minus_1 = m - 1 (so
+// m = 2^64 is representable).  Exact 64-bit remainders (the sketch kernels
+// draw with m <= 65536 through perm_draw).
+__global__ void randint_general_kernel(const u64* pseeds, const u64* elems, const u64* steps,
+                                       const u64* m_minus_1, int64_t n, u64* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u64 key = pseeds[i] + elems[i] * K_ELEM + steps[i] * K_STEP;
+  const u64 mm1 = m_minus_1[i];
+  u64 x = mix64(key);
+  if (mm1 == ~0ull) {  // m = 2^64: every x is accepted, x mod 2^64 = x
+    out[i] = x;
+    return;
+  }
+  const u64 m = mm1 + 1;
+  const u64 r = (~0ull % m + 1) % m;  // 2^64 mod m
+  for (u64 attempt = 1; r != 0 && x > ~0ull - r; ++attempt) x = mix64(key + attempt * K_RETRY);
+  out[i] = x % m;
 }
 
 // ---- arithmetic self-check: ddiv_fast == __ddiv_rn on the fast range, and

@@ -114,17 +114,22 @@ def perm_draw_batch(perm_seeds, elements, steps, ks) -> np.ndarray:
 
 
 def rand_int_between(scheme: SeedScheme, element: int, step: int, lo: int, hi: int) -> int:
-    """Unbiased integer in [lo, hi] (randgen.py:122-143), hi - lo < 65536."""
+    """Unbiased integer in [lo, hi] (randgen.py:122-143), any range up to
+    2**64 wide, drawn on the device (gm_rand_int_between_batch)."""
     if step < 1:
         raise ValueError(f"step must be >= 1, got {step}")
     if hi < lo:
         raise ValueError(f"empty range [{lo}, {hi}]")
     m = hi - lo + 1
-    if m > 65536:
-        raise ValueError("ranges wider than 65536 are outside the device draw")
-    # the device draw is z + (g mod m) with m = k - z + 1; key is (element, step)
-    j = perm_draw_batch([scheme.perm_seed], [element], [step], [step + m - 1])[0]
-    return lo + int(j) - step
+    if m > 1 << 64:
+        # the reference's rejection bound 2**64 - 2**64 % m is 0 here: it never returns
+        raise ValueError("ranges wider than 2**64 have no accepted draw")
+    dev = _device.require_cuda()
+    t = lambda v: _u64_tensor([v & ((1 << 64) - 1)], dev)  # noqa: E731
+    out = torch.empty(1, dtype=torch.int64, device=dev)
+    _device.call("gm_rand_int_between_batch", t(scheme.perm_seed).data_ptr(), t(element).data_ptr(),
+                 t(step).data_ptr(), t(m - 1).data_ptr(), 1, out.data_ptr(), _device.stream_ptr())
+    return lo + (int(out.cpu().item()) & ((1 << 64) - 1))
 
 
 class ElementQueueState:

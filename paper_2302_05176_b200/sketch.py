@@ -11,12 +11,11 @@ Generators run on the device:
                                          run to k (GM_FLAG_EXHAUSTIVE)
   sketch_csr / sketch_many            -> batched K1 over CSR arrays (new; the
                                          reference callers loop per vector)
-Registers equal the reference's: s bit-exact; y within the documented
-tolerance (the device log is CUDA's, not glibc's), and
-bit-identical after the exact-y finalize (exact_y_host, gm_exact_y), which
-the reference-typed entry points (sketch_fast/naive, sketch_stream,
-sketch_pairs) always apply so GumbelMaxSketch equality holds against the
-reference's own sketches.
+Registers equal the reference's bit for bit, s and y: the device log is a
+clone of glibc's (the reference's math.log; csrc/gm_glibc_log.cuh), so
+GumbelMaxSketch equality holds against the reference's own sketches with no
+host pass.  (exact_y_host, the host re-derivation of y from the winners, is
+kept as a cross-check.)
 The *_counted work counters count arrivals the device computed, which is
 schedule-dependent and differs from the reference's FastSearch count.
 """
@@ -199,17 +198,17 @@ def _check_k(k: int) -> None:
 
 
 def sketch_csr(ids, weights, offsets, k: int, scheme: SeedScheme, *, exhaustive: bool = False,
-               counted: bool = False, asynchronous: bool = False, split: bool = False,
+               counted: bool = False, asynchronous: bool = False,
                exact_y: bool = False) -> SketchBatch:
     """Sketch every CSR vector ids[offsets[v]:offsets[v+1]] on the device.
 
     ids: uint32/uint64 (or int32/int64 viewed as unsigned) tensor or array;
     weights: float32/float64; offsets: int64 [n_vec + 1].  Ids must be
     distinct within a vector (WeightedVector keys).  Device tensors are used
-    in place; host arrays are copied in.  ``split=True`` selects the
-    experimental split schedule; results are identical.
+    in place; host arrays are copied in.
     ``exact_y=True`` re-derives y on the host with the reference's
-    arithmetic (exact_y_host): bit-identical y, at host cost."""
+    arithmetic (exact_y_host; a cross-check -- the device y is already
+    bit-identical)."""
     _check_k(k)
     dev = _device.require_cuda()
     ids_t = ids if isinstance(ids, torch.Tensor) else torch.from_numpy(_as_id_np(ids))
@@ -223,8 +222,7 @@ def sketch_csr(ids, weights, offsets, k: int, scheme: SeedScheme, *, exhaustive:
     y = torch.empty((n_vec, k), dtype=torch.float64, device=dev)
     s = torch.empty((n_vec, k), dtype=torch.int64, device=dev)
     em = torch.empty(n_vec, dtype=torch.int64, device=dev) if counted else None
-    flags = ((_lib.GM_FLAG_EXHAUSTIVE if exhaustive else 0) | (_lib.GM_FLAG_ASYNC if asynchronous else 0)
-             | (_lib.GM_FLAG_SPLIT if split else 0))
+    flags = (_lib.GM_FLAG_EXHAUSTIVE if exhaustive else 0) | (_lib.GM_FLAG_ASYNC if asynchronous else 0)
     _device.call("gm_sketch_csr", ids_t.data_ptr(), _device.id_bits_of(ids_t), w_t.data_ptr(),
                  _device.w_bits_of(w_t), off_t.data_ptr(), n_vec, k, scheme.global_seed,
                  scheme.stream_salt, flags, y.data_ptr(), s.data_ptr(), _device.ptr(em),
@@ -289,9 +287,9 @@ def sketch_csr_host(ids, weights, offsets, k: int, scheme: SeedScheme, *, out=No
 
 def exact_y_host(ids, weights, offsets, k: int, scheme: SeedScheme, s, y, threads: int = 0):
     """Re-derive registers' values with the reference's arithmetic (glibc log,
-    randgen.py:158-207) from their winning elements, in place: y becomes
-    bit-identical to the reference's (gm_exact_y; host arrays, no device
-    work).  s: uint64/int64 [n_vec, k] (or [k]), y: float64 of the same
+    randgen.py:158-207) from their winning elements, in place (gm_exact_y;
+    host arrays, no device work).  A cross-check of the device registers,
+    which already carry these bits; no generator calls it.  s: uint64/int64 [n_vec, k] (or [k]), y: float64 of the same
     shape; CPU tensors or numpy arrays."""
     def np_of(a):
         return a.numpy() if isinstance(a, torch.Tensor) else a
@@ -325,9 +323,9 @@ def sketch_csr_host_many(batches, k: int, scheme: SeedScheme, *, streams: int = 
     are taken from the generator (copy them to keep them longer)."""
     _check_k(k)
     dev = _device.require_cuda()
-    pool = [torch.cuda.Stream(device=dev) for _ in range(max(1, streams))]
+    pool = _device.stream_pool(dev, max(1, streams))
     inflight = []  # (stream index, y, s, keep-alive inputs)
-    outs = {}
+    outs = {}  # output set -> page-locked (y, s) flat buffers, grown when a batch needs more
 
     staging = {}  # per stream: page-locked input buffers, reused (grown when needed)
 
@@ -358,11 +356,13 @@ def sketch_csr_host_many(batches, k: int, scheme: SeedScheme, *, streams: int = 
         t_off = off if isinstance(off, torch.Tensor) else np.ascontiguousarray(np.asarray(off, dtype=np.int64))
         t_ids, t_w, t_off = pinned(j, "ids", t_ids), pinned(j, "w", t_w), pinned(j, "off", t_off)
         n_vec = t_off.numel() - 1
-        key = (i % (2 * len(pool)), n_vec)  # two output sets per stream: a result outlives `streams` more yields
-        if key not in outs:
-            outs[key] = (torch.empty((n_vec, k), dtype=torch.float64).pin_memory(),
-                         torch.empty((n_vec, k), dtype=torch.int32 if s32 else torch.int64).pin_memory())
-        y, s = outs[key]
+        key = i % (2 * len(pool))  # two output sets per stream: a result outlives `streams` more yields
+        yb, sb = outs.get(key, (None, None))
+        if yb is None or yb.numel() < n_vec * k:
+            yb = torch.empty(max(n_vec * k, 1), dtype=torch.float64).pin_memory()
+            sb = torch.empty(max(n_vec * k, 1), dtype=torch.int32 if s32 else torch.int64).pin_memory()
+            outs[key] = (yb, sb)
+        y, s = yb[: n_vec * k].view(n_vec, k), sb[: n_vec * k].view(n_vec, k)
         flags = _lib.GM_FLAG_ASYNC | (_lib.GM_FLAG_S32 if s32 else 0)
         _device.call("gm_sketch_csr_host", t_ids.data_ptr(), id_bits, t_w.data_ptr(), w_bits, t_off.data_ptr(), n_vec,
                      k, scheme.global_seed, scheme.stream_salt, flags, y.data_ptr(), s.data_ptr(), None,
@@ -457,9 +457,7 @@ def _sketch_vector(v: WeightedVector, params: GenerationParams, exhaustive: bool
     off = np.array([0, ids.size], dtype=np.int64)
     if v.n_plus > LARGE_VECTOR:
         y, s, em = sketch_elements(ids, w, k, params.scheme, exhaustive=exhaustive)
-        y, s = y.cpu().numpy(), s.cpu().numpy()
-        exact_y_host(ids, w, off, k, params.scheme, s, y)
-        return _to_sketch(k, y, s, params.scheme.fingerprint), em
+        return _to_sketch(k, y.cpu().numpy(), s.cpu().numpy(), params.scheme.fingerprint), em
     _device.require_cuda()
     bits = 32 if (ids.size and int(ids.max()) < (1 << 32)) else 64
     ids_h = ids.astype(np.uint32) if bits == 32 else ids
@@ -470,7 +468,6 @@ def _sketch_vector(v: WeightedVector, params: GenerationParams, exhaustive: bool
     _device.call("gm_sketch_csr_host", ids_h.ctypes.data, bits, w.ctypes.data, 64, off.ctypes.data, 1,
                  k, params.scheme.global_seed, params.scheme.stream_salt, flags, y.ctypes.data,
                  s.ctypes.data, em.ctypes.data, _device.stream_ptr())
-    exact_y_host(ids_h, w, off, k, params.scheme, s, y)
     return _to_sketch(k, y, s, params.scheme.fingerprint), int(em[0])
 
 
@@ -495,9 +492,9 @@ def sketch_fast_counted(v: WeightedVector, params: GenerationParams):
 
 
 def sketch_many(vectors: Sequence[WeightedVector], params: GenerationParams,
-                exact_y: bool = True) -> list[GumbelMaxSketch]:
-    """Sketch a list of vectors in one batched launch (y re-derived with the
-    reference's arithmetic unless ``exact_y=False``)."""
+                exact_y: bool = False) -> list[GumbelMaxSketch]:
+    """Sketch a list of vectors in one batched launch (``exact_y``: see
+    sketch_csr)."""
     if not vectors:
         return []
     for v in vectors:

@@ -106,12 +106,6 @@ def stream_finalize(state: StreamSketchState) -> GumbelMaxSketch:
     if state._unset > 0:
         raise IncompleteSketchError([j for j in range(state.k) if math.isinf(y[j])])
     s = state._s.cpu().numpy().view(np.uint64)
-    # y with the reference's arithmetic: the winners' weights are in the
-    # id -> weight dict the stream checks keep
-    win = np.unique(s)
-    wmap = {e & _MASK64: wt for e, wt in state.weights.items()}
-    exact_y_host(win, np.array([wmap[int(e)] for e in win], np.float64), np.array([0, win.size], np.int64),
-                 state.k, state.scheme, s, y)
     alias = state._alias
     s_out = tuple(alias.get(int(x), int(x)) for x in s)
     return GumbelMaxSketch(state.k, s_out, tuple(y.tolist()), state.scheme.fingerprint)
@@ -126,7 +120,7 @@ def sketch_stream(items: Iterable[StreamItem], k: int, scheme: SeedScheme,
     return stream_finalize(state)
 
 
-def sketch_pairs(ids, weights, k: int, scheme: SeedScheme, check: bool = True, exact_y: bool = True,
+def sketch_pairs(ids, weights, k: int, scheme: SeedScheme, check: bool = True, exact_y: bool = False,
                  skip_duplicates: bool = True):
     """Bulk stream of (id, weight) arrays, checked and sketched on the device.
 
@@ -135,9 +129,9 @@ def sketch_pairs(ids, weights, k: int, scheme: SeedScheme, check: bool = True, e
     InconsistentWeightError for an id that reappears with another weight,
     raised for the first offending item like stream_update.  With
     ``skip_duplicates`` only first occurrences are sketched (duplicates are
-    register no-ops; stream.py:74-78).  ``exact_y`` (default) re-derives y
-    with the reference's arithmetic (sketch.exact_y_host).  Returns a
-    GumbelMaxSketch."""
+    register no-ops; stream.py:74-78).  ``exact_y`` re-derives y on the host
+    (sketch.exact_y_host, a cross-check: the device y is already the
+    reference's).  Returns a GumbelMaxSketch."""
     a_ids, id_bits = _device.id_array(ids)
     a_w, w_bits = _device.weight_array(weights)
     dev = _device.require_cuda()
