@@ -50,6 +50,7 @@ extern "C" {
 #define GM_ERR_MISMATCHED 6         /* MismatchedSketchError   sketch.py:314-322   */
 #define GM_ERR_CUDA 100             /* CUDA runtime failure (no reference class)   */
 #define GM_ERR_NO_DEVICE 101        /* no sm_100 device visible                     */
+#define GM_ERR_COMM 102             /* NCCL missing or a collective failed          */
 
 /* flags */
 #define GM_FLAG_ASYNC 0x1u       /* enqueue only; see gm_stream_status()           */
@@ -57,6 +58,36 @@ extern "C" {
 #define GM_FLAG_ACCUMULATE 0x4u  /* gm_sketch_elements: fold into y_io/s_io        */
 /* 0x8u: reserved (was an experimental split schedule, removed) */
 #define GM_FLAG_S32 0x10u        /* gm_sketch_csr_host: s_out is uint32 (32-bit ids) */
+#define GM_FLAG_ONE_VECTOR 0x20u /* gm_sketch_csr_seeded: n_vec sketches of ONE vector */
+
+/*
+ * Multi-GPU register exchange (configs 4-5 sharded by element over N GPUs of
+ * one node).  The reference's distributed form is "sketch
+ * per site, merge centrally" (merge = estimate.py:103-125);
+ * here every rank sketches its contiguous shard with gm_sketch_elements and
+ * the k registers are combined in place over NCCL (NVLink / NVSwitch).
+ * NCCL is opened at run time (libnccl.so.2); without it these return
+ * GM_ERR_COMM and everything else still works.
+ *   gm_comm_unique_id   rank 0 makes the id (gm_comm_id_bytes() bytes) and
+ *                       shares it out of band (e.g. a torch.distributed
+ *                       broadcast)
+ *   gm_comm_init        one communicator per rank on the current device
+ *   gm_allreduce_min_registers    two NCCL all-reduces with MIN (y; then
+ *                       the ids of the ranks holding the minimum): the
+ *                       register-wise (y, id) minimum -- smaller id wins a tie
+ *                       of equal y (sketch.py:196-205)
+ *   gm_allgather_merge_registers  NCCL all-gather of every rank's registers +
+ *                       the device merge in rank order: merge([rank0, rank1,
+ *                       ...]) exactly (earlier rank wins ties)
+ * y (device, double[k]) and s (device, uint64[k]) are read and overwritten
+ * with the merged sketch on every rank; enqueued on `stream`.
+ */
+int gm_comm_id_bytes(void);
+int gm_comm_unique_id(void *id_out);
+int gm_comm_init(const void *id, int nranks, int rank, void **comm_out);
+int gm_comm_destroy(void *comm);
+int gm_allreduce_min_registers(void *comm, double *y, uint64_t *s, int32_t k, void *stream);
+int gm_allgather_merge_registers(void *comm, double *y, uint64_t *s, int32_t k, void *stream);
 
 /* Library version (major*10000 + minor*100 + patch). */
 int gm_version(void);
@@ -103,13 +134,31 @@ int gm_sketch_csr(const void *ids, int id_bits, const void *w, int w_bits,
                   double *y_out, uint64_t *s_out, int64_t *emitted_out,
                   void *stream);
 
+/* gm_sketch_csr with a global seed per vector (device array global_seeds[n_vec];
+ * permutation seed = global_seeds[v] ^ stream_salt, as SeedScheme does,
+ * randgen.py:72-95): one launch sketches the same vector under R seeds (R
+ * independent sketches, e.g. for estimator variance) or a batch whose
+ * vectors carry their own schemes.  With GM_FLAG_ONE_VECTOR, offsets holds
+ * just [lo, hi] and all n_vec sketches are of that one vector (one per
+ * seed; the vector is read once from HBM/L2, not replicated).  Needs k <=
+ * the shared-memory register limit (k <= 4096 at 16 B per register, two
+ * slots). */
+int gm_sketch_csr_seeded(const void *ids, int id_bits, const void *w, int w_bits,
+                         const int64_t *offsets, int64_t n_vec, int32_t k,
+                         const uint64_t *global_seeds, uint64_t stream_salt,
+                         uint32_t flags, double *y_out, uint64_t *s_out,
+                         int64_t *emitted_out, void *stream);
+
 /* Same contract with HOST buffers; copies in and out inside the call (page-
  * locked outputs are stored by the kernel directly).  With GM_FLAG_ASYNC the
  * call only enqueues: the caller keeps the buffers untouched until `stream`
  * is synchronised.  Alternating two streams pipelines batches: one batch's
  * input copy and first CTAs overlap the previous batch's tail.  With
  * GM_FLAG_S32 (32-bit ids only) s_out points to uint32 ids (an unset register
- * reads 0xFFFFFFFF): 12 instead of 16 bytes per register cross the bus. */
+ * reads 0xFFFFFFFF): 12 instead of 16 bytes per register cross the bus.
+ * A synchronous call with ONE vector of >= 4096 elements (GM_SINGLE_GRID_MIN)
+ * runs on the grid-wide kernels of gm_sketch_elements (every SM) instead of
+ * one CTA; same registers. */
 int gm_sketch_csr_host(const void *ids, int id_bits, const void *w, int w_bits,
                        const int64_t *offsets, int64_t n_vec, int32_t k,
                        uint64_t global_seed, uint64_t stream_salt,
@@ -264,10 +313,13 @@ int gm_stats_read(unsigned long long *out16);
 int gm_trace_read(unsigned long long *ev_out, unsigned *n_out);
 
 /* Diagnostics.
- * gm_probe_arrival_rate: n_threads threads each emit `iters` exact arrivals
- * (spacing + permutation draw, no pruning or registers); the measured rate
- * is the compute roofline of the sketch kernels.  sink: 1
- * device double.  Asynchronous.
+ * gm_probe_arrival_rate: n_threads threads each walk C element queues for
+ * `iters` exact arrivals apiece (iters | C << 24, C = 1, 2 or 4; C = 0 means
+ * 2), with the lane step's own arithmetic (uniform hash, glibc-clone log from
+ * a shared-memory table, rounded product, branch-free divide, prefix add,
+ * permutation hash + 64-bit Barrett reduction) and no pruning, tables or
+ * registers; the measured rate is the compute roofline of the sketch kernels
+ * (DESIGN.md).  sink: 1 device double.  Asynchronous.
  * gm_count_arrivals_csr: counts[v] = number of arrivals t <= tau[v] over the
  * elements of CSR vector v (device arrays); the algorithmic survivor count.
  * Synchronises `stream`. */

@@ -186,3 +186,42 @@ def log_uniforms(seed: int, i0: int, n: int):
     lg = np.empty(n, np.float64)
     lib().gmo_log_uniforms(seed & MASK64, i0, n, _p(u), _p(lg))
     return u, lg
+
+
+def sketch_stream_chunked(ids, w, k, seed, salt=DEFAULT_STREAM_SALT, threads=0, chunk=1 << 23):
+    """sketch_stream (stream.py:143-153) of a large element set, run as
+    contiguous chunks of `chunk` items sketched on all host threads (ctypes
+    releases the GIL) and merged in chunk order -- the partition law
+    (estimate.py:103-125, test_estimate.py:174-199): equal to one
+    sketch_stream of the whole when duplicates carry equal weights.  Each
+    worker widens its own chunk to u64 ids / f64 weights, so the whole set is
+    never copied.  Returns (rc, y, s)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    n = len(ids)
+    bounds = list(range(0, n, chunk)) + [n]
+    threads = threads or min(32, os.cpu_count() or 1)
+
+    def one(c):
+        a, b = bounds[c], bounds[c + 1]
+        rc, y, s, _, _ = sketch_stream(ids[a:b], w[a:b], k, seed, salt)
+        return rc, y, s
+
+    with ThreadPoolExecutor(threads) as ex:
+        parts = list(ex.map(one, range(len(bounds) - 1)))
+    rc = next((p[0] for p in parts if p[0] not in (OK, INCOMPLETE)), OK)
+    if rc != OK:
+        return rc, None, None
+    y, s = merge(np.stack([p[1] for p in parts]), np.stack([p[2] for p in parts]))
+    return (INCOMPLETE if np.isinf(y).any() else OK), y, s
+
+
+def digest(y, s) -> str:
+    """sha256 of the registers: y as IEEE doubles then s as uint64, little-endian."""
+    import hashlib
+
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(y, dtype="<f8").tobytes())
+    h.update(np.ascontiguousarray(s, dtype="<u8").tobytes())
+    return h.hexdigest()

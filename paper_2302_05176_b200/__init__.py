@@ -58,6 +58,8 @@ from .sketch import (
     check_compatible,
     compute_ri,
     sketch_csr,
+    sketch_csr_seeded,
+    sketch_vector_seeds,
     sketch_csr_host,
     sketch_csr_host_many,
     exact_y_host,

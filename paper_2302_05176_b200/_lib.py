@@ -23,11 +23,13 @@ GM_ERR_INCOMPLETE = 5
 GM_ERR_MISMATCHED = 6
 GM_ERR_CUDA = 100
 GM_ERR_NO_DEVICE = 101
+GM_ERR_COMM = 102
 
 GM_FLAG_ASYNC = 0x1
 GM_FLAG_EXHAUSTIVE = 0x2
 GM_FLAG_ACCUMULATE = 0x4
 GM_FLAG_S32 = 0x10
+GM_FLAG_ONE_VECTOR = 0x20
 
 # every symbol include/gmsketch_b200.h declares: (name, restype, argtypes)
 _u64, _i64, _i32, _u32, _int, _vp, _dbl = (ctypes.c_uint64, ctypes.c_int64, ctypes.c_int32,
@@ -40,10 +42,17 @@ SIGNATURES = {
     "gm_stats_read": (_int, [_vp]),
     "gm_trace_read": (_int, [_vp, _vp]),
     "gm_stream_status": (_int, [_vp]),
+    "gm_comm_id_bytes": (_int, []),
+    "gm_comm_unique_id": (_int, [_vp]),
+    "gm_comm_init": (_int, [_vp, _int, _int, _vp]),
+    "gm_comm_destroy": (_int, [_vp]),
+    "gm_allreduce_min_registers": (_int, [_vp, _vp, _vp, _i32, _vp]),
+    "gm_allgather_merge_registers": (_int, [_vp, _vp, _vp, _i32, _vp]),
     "gm_release_stream": (_int, [_vp]),
     "gm_finalize": (_int, []),
     "gm_workspace_count": (_int, []),
     "gm_sketch_csr": (_int, [_vp, _int, _vp, _int, _vp, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),
+    "gm_sketch_csr_seeded": (_int, [_vp, _int, _vp, _int, _vp, _i64, _i32, _vp, _u64, _u32, _vp, _vp, _vp, _vp]),
     "gm_sketch_csr_host": (_int, [_vp, _int, _vp, _int, _vp, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),
     "gm_sketch_elements": (_int, [_vp, _int, _vp, _int, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),
     "gm_sketch_elements_host": (_int, [_vp, _int, _vp, _int, _i64, _i32, _u64, _u64, _u32, _vp, _vp, _vp, _vp]),

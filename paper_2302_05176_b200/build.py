@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libgmsketch_b200.so")
 SOURCES = [os.path.join(CSRC, "gm_capi.cu"), os.path.join(CSRC, "gm_exact.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("gm_core.cuh", "gm_walk.cuh", "gm_kernels.cuh", "gm_csr.cuh",
-                                                  "gm_pairs.cuh", "gm_glibc_log.cuh", "gm_glibc_logtab.h")] + [
+                                                  "gm_pairs.cuh", "gm_comm.cuh", "gm_glibc_log.cuh", "gm_glibc_logtab.h")] + [
     os.path.join(os.path.dirname(HERE), "include", "gmsketch_b200.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -35,7 +35,7 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT, *SOURCES, "-lcudart"]
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT, *SOURCES, "-lcudart", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

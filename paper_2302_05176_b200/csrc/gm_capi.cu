@@ -19,6 +19,7 @@
 #include "../../include/gmsketch_b200.h"
 #include "gm_csr.cuh"
 #include "gm_pairs.cuh"
+#include "gm_comm.cuh"
 
 #include <cub/device/device_scan.cuh>
 
@@ -59,10 +60,6 @@ struct Workspace {
   size_t dense_cap = 0;
   u32* csr_dense = nullptr;                // CSR warp-walker dense arrays (stamped)
   size_t csr_dense_cap = 0;
-  double* vsum = nullptr;                  // per-vector total weight (CSR prep)
-  size_t vsum_cap = 0;
-  int* vflag = nullptr;                    // per-vector flags (CSR prep)
-  size_t vflag_cap = 0;
   Surv* surv = nullptr;                    // K2 filter survivors (id, weight)
   size_t surv_cap = 0;
   unsigned long long* sample_set = nullptr;  // K2 weight-sample id set
@@ -83,7 +80,7 @@ std::map<std::pair<int, cudaStream_t>, Workspace*> g_ws;
 // Frees a workspace (the caller has synchronised its stream).
 void free_ws(Workspace* w) {
   void* dev_ptrs[] = {w->counters, w->err, w->ull, w->dbl, w->regs, w->heavy, w->dense, w->csr_dense,
-                      w->vsum, w->vflag, w->surv, w->sample_set, w->sample_part, w->stage, w->pt_keys,
+                      w->surv, w->sample_set, w->sample_part, w->stage, w->pt_keys,
                       w->pt_first};
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
@@ -178,8 +175,8 @@ using CsrSmallK = CsrCfg<256, 16, 4, 2, 75, 4>;
 
 template <class C, class IdT, class WT>
 int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k,
-               u64 useed, u64 pseed, double* y, u64* s, int64_t* em, Workspace* ws,
-               cudaStream_t st, int attempt0, const int* vec_list = nullptr, bool skip_prep = false) {
+               u64 useed, u64 salt, const u64* vseeds, int one_vec, double* y, u64* s, int64_t* em, Workspace* ws,
+               cudaStream_t st, int attempt0) {
   auto kern = csr3_kernel<C, IdT, WT>;
   const size_t smem = csr3_smem_bytes<C>(k);
   int per_sm = 0;
@@ -217,25 +214,12 @@ int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n
   // own scratch: the K2 heavy kernel relies on ws->dense staying zeroed
   int rc = grow(&ws->csr_dense, &ws->csr_dense_cap, (size_t)grid * C::NWARP * k, st);
   if (rc) return rc;
-  rc = grow(&ws->vsum, &ws->vsum_cap, (size_t)n_vec, st);
-  if (rc) return rc;
-  rc = grow(&ws->vflag, &ws->vflag_cap, (size_t)n_vec, st);
-  if (rc) return rc;
   CK(cudaMemsetAsync(ws->counters, 0, sizeof(int), st));
-  // the slots compute each vector's weight sum themselves (no prep launch)
-  // unless a vector subset re-uses sums computed earlier (skip_prep), or
-  // GM_CSR_PREP=1 asks for the separate prep kernel
-  static const bool prep_kernel = getenv("GM_CSR_PREP") && atoi(getenv("GM_CSR_PREP")) == 1;
-  const bool inkernel = !skip_prep && !prep_kernel;
-  if (!skip_prep && prep_kernel) {
-    const int64_t prep_blocks = std::min<int64_t>((n_vec + 7) / 8, (int64_t)num_sms() * 16);
-    csr_prep_kernel<WT><<<(unsigned)prep_blocks, 256, 0, st>>>((const WT*)w, offsets, n_vec, ws->vsum, ws->vflag,
-                                                               ws->err);
-    CK(cudaGetLastError());
-  }
-  kern<<<(unsigned)grid, C::NT, smem, st>>>((const IdT*)ids, (const WT*)w, offsets, n_vec, k, useed, pseed,
-                                            inkernel ? nullptr : ws->vsum, inkernel ? nullptr : ws->vflag, y, s, em,
-                                            ws->counters, ws->csr_dense, ws->err, attempt0, vec_list);
+  // the slots compute each vector's weight sum, validate its weights and check
+  // the divide range themselves when they load it (no prep launch)
+  kern<<<(unsigned)grid, C::NT, smem, st>>>((const IdT*)ids, (const WT*)w, offsets, n_vec, k, useed, salt, vseeds,
+                                            one_vec, nullptr, nullptr, y, s, em, ws->counters, ws->csr_dense, ws->err,
+                                            attempt0, nullptr);
   CK(cudaGetLastError());
   return GM_OK;
 }
@@ -573,6 +557,113 @@ int gm_workspace_count(void) {
   return (int)g_ws.size();
 }
 
+// ---- NCCL register exchange (gm_comm.cuh) ----
+#define NK(call)                                                                                     \
+  do {                                                                                               \
+    ncclResult_t r_ = (call);                                                                        \
+    if (r_ != ncclSuccess) return fail(GM_ERR_COMM, "%s failed: %s", #call, nccl_api().error_string(r_)); \
+  } while (0)
+
+static int comm_api_ok() {
+  NcclApi& a = nccl_api();
+  return a.ok ? GM_OK : fail(GM_ERR_COMM, "%s", a.why);
+}
+
+int gm_comm_unique_id(void* id_out) {
+  g_msg[0] = 0;
+  int rc = comm_api_ok();
+  if (rc) return rc;
+  if (!id_out) return fail(GM_ERR_INVALID_PARAMETER, "id_out is NULL");
+  ncclUniqueId id;
+  NK(nccl_api().get_unique_id(&id));
+  memcpy(id_out, &id, sizeof(id));
+  return GM_OK;
+}
+
+int gm_comm_id_bytes(void) { return (int)sizeof(ncclUniqueId); }
+
+int gm_comm_init(const void* id, int nranks, int rank, void** comm_out) {
+  g_msg[0] = 0;
+  int rc = comm_api_ok();
+  if (rc) return rc;
+  if (!id || !comm_out || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(GM_ERR_INVALID_PARAMETER, "gm_comm_init: bad arguments (nranks %d, rank %d)", nranks, rank);
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  GmComm* c = new GmComm();
+  CK(cudaGetDevice(&c->device));
+  c->nranks = nranks;
+  c->rank = rank;
+  const ncclResult_t r = nccl_api().comm_init_rank(&c->comm, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(GM_ERR_COMM, "ncclCommInitRank failed: %s", nccl_api().error_string(r));
+  }
+  *comm_out = c;
+  return GM_OK;
+}
+
+int gm_comm_destroy(void* comm) {
+  g_msg[0] = 0;
+  if (!comm) return GM_OK;
+  GmComm* c = (GmComm*)comm;
+  if (c->ybuf) cudaFree(c->ybuf);
+  if (c->sbuf) cudaFree(c->sbuf);
+  if (c->comm && nccl_api().ok) NK(nccl_api().comm_destroy(c->comm));
+  delete c;
+  return GM_OK;
+}
+
+static int comm_scratch(GmComm* c, size_t regs) {
+  if (c->cap >= regs) return GM_OK;
+  if (c->ybuf) CK(cudaFree(c->ybuf));
+  if (c->sbuf) CK(cudaFree(c->sbuf));
+  c->ybuf = nullptr;
+  c->sbuf = nullptr;
+  c->cap = 0;
+  CK(cudaMalloc(&c->ybuf, regs * sizeof(double)));
+  CK(cudaMalloc(&c->sbuf, regs * sizeof(u64)));
+  c->cap = regs;
+  return GM_OK;
+}
+
+int gm_allreduce_min_registers(void* comm, double* y, uint64_t* s, int32_t k, void* stream) {
+  g_msg[0] = 0;
+  (void)cudaGetLastError();
+  int rc = comm_api_ok();
+  if (rc) return rc;
+  if (!comm || k < 1) return fail(GM_ERR_INVALID_PARAMETER, "gm_allreduce_min_registers: bad arguments");
+  GmComm* c = (GmComm*)comm;
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((rc = comm_scratch(c, (size_t)k))) return rc;
+  NK(nccl_api().all_reduce(y, c->ybuf, (size_t)k, ncclFloat64, ncclMin, c->comm, st));
+  mask_min_ids_kernel<<<(unsigned)std::min<int64_t>(((int64_t)k + 255) / 256, 1024), 256, 0, st>>>(y, c->ybuf, s,
+                                                                                                   c->sbuf, (u32)k);
+  CK(cudaGetLastError());
+  NK(nccl_api().all_reduce(c->sbuf, s, (size_t)k, ncclUint64, ncclMin, c->comm, st));
+  CK(cudaMemcpyAsync(y, c->ybuf, (size_t)k * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  return GM_OK;
+}
+
+int gm_allgather_merge_registers(void* comm, double* y, uint64_t* s, int32_t k, void* stream) {
+  g_msg[0] = 0;
+  (void)cudaGetLastError();
+  int rc = comm_api_ok();
+  if (rc) return rc;
+  if (!comm || k < 1) return fail(GM_ERR_INVALID_PARAMETER, "gm_allgather_merge_registers: bad arguments");
+  GmComm* c = (GmComm*)comm;
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((rc = comm_scratch(c, (size_t)k * c->nranks))) return rc;
+  NK(nccl_api().group_start());
+  NK(nccl_api().all_gather(y, c->ybuf, (size_t)k, ncclFloat64, c->comm, st));
+  NK(nccl_api().all_gather(s, c->sbuf, (size_t)k, ncclUint64, c->comm, st));
+  NK(nccl_api().group_end());
+  const unsigned grid = (unsigned)std::min<int64_t>(((int64_t)k + 255) / 256, 4096);
+  merge_kernel<<<grid, 256, 0, st>>>(c->ybuf, c->sbuf, c->nranks, (u32)k, y, s);
+  CK(cudaGetLastError());
+  return GM_OK;
+}
+
 int gm_stream_status(void* stream) {
   Workspace* ws = nullptr;
   int rc = get_ws((cudaStream_t)stream, &ws);
@@ -619,43 +710,104 @@ static int csr_by_elements(const void* ids, int id_bits, const void* w, int w_bi
   return rc;
 }
 
+// The batched K1 launch (csr3_kernel) for every id/weight width; vseeds
+// (device, nullable): per-vector global seeds.
+static int csr_dispatch(const void* ids, int id_bits, const void* w, int w_bits, const int64_t* offsets,
+                        int64_t n_vec, int32_t k, uint64_t global_seed, uint64_t stream_salt, const uint64_t* vseeds,
+                        uint32_t flags, double* y_out, uint64_t* s_out, int64_t* emitted_out, cudaStream_t st) {
+  int rc = check_common(id_bits, w_bits, k);
+  if (rc) return rc;
+  if (n_vec < 0) return fail(GM_ERR_INVALID_PARAMETER, "n_vec must be >= 0");
+  if (n_vec == 0) return GM_OK;
+  Workspace* ws = nullptr;
+  rc = get_ws(st, &ws);
+  if (rc) return rc;
+  const u64 useed = global_seed, salt = stream_salt;
+  const u32 kk = (u32)k;
+  const bool small_k = kk <= 512;  // CsrSmallK: four vector slots
+  const int one_vec = (flags & GM_FLAG_ONE_VECTOR) ? 1 : 0;
+  if (one_vec && !vseeds) return fail(GM_ERR_INVALID_PARAMETER, "GM_FLAG_ONE_VECTOR needs per-sketch seeds");
+  // exhaustive = a single pass with tau = +inf (pass_tau's last attempt)
+  const int a0 = (flags & GM_FLAG_EXHAUSTIVE) ? 3 : 0;
+#define GM_CSR_LAUNCH(I, W)                                                                                          \
+  rc = small_k ? launch_csr<CsrSmallK, I, W>(ids, w, offsets, n_vec, kk, useed, salt, vseeds, one_vec, y_out,     \
+                                             s_out, emitted_out, ws, st, a0)                                         \
+               : launch_csr<CsrDefault, I, W>(ids, w, offsets, n_vec, kk, useed, salt, vseeds, one_vec, y_out,    \
+                                              s_out, emitted_out, ws, st, a0)
+  if (id_bits == 32 && w_bits == 32) GM_CSR_LAUNCH(u32, float);
+  else if (id_bits == 32) GM_CSR_LAUNCH(u32, double);
+  else if (w_bits == 32) GM_CSR_LAUNCH(u64, float);
+  else GM_CSR_LAUNCH(u64, double);
+#undef GM_CSR_LAUNCH
+  if (rc == -1) {
+    if (vseeds) return fail(GM_ERR_INVALID_PARAMETER, "per-sketch seeds need k small enough for shared-memory registers");
+    return csr_by_elements(ids, id_bits, w, w_bits, offsets, n_vec, k, global_seed, stream_salt, flags, y_out, s_out,
+                           emitted_out, st);
+  }
+  if (rc) return rc;
+  if (flags & GM_FLAG_ASYNC) return GM_OK;
+  return check_sync(ws, st);
+}
+
 int gm_sketch_csr(const void* ids, int id_bits, const void* w, int w_bits, const int64_t* offsets,
                   int64_t n_vec, int32_t k, uint64_t global_seed, uint64_t stream_salt,
                   uint32_t flags, double* y_out, uint64_t* s_out, int64_t* emitted_out,
                   void* stream) {
   g_msg[0] = 0;
   (void)cudaGetLastError();
-  int rc = check_common(id_bits, w_bits, k);
+  return csr_dispatch(ids, id_bits, w, w_bits, offsets, n_vec, k, global_seed, stream_salt, nullptr, flags, y_out,
+                      s_out, emitted_out, (cudaStream_t)stream);
+}
+
+int gm_sketch_csr_seeded(const void* ids, int id_bits, const void* w, int w_bits, const int64_t* offsets,
+                         int64_t n_vec, int32_t k, const uint64_t* global_seeds, uint64_t stream_salt,
+                         uint32_t flags, double* y_out, uint64_t* s_out, int64_t* emitted_out, void* stream) {
+  g_msg[0] = 0;
+  (void)cudaGetLastError();
+  if (!global_seeds) return fail(GM_ERR_INVALID_PARAMETER, "global_seeds must be a device array of n_vec seeds");
+  return csr_dispatch(ids, id_bits, w, w_bits, offsets, n_vec, k, 0, stream_salt, global_seeds, flags, y_out, s_out,
+                      emitted_out, (cudaStream_t)stream);
+}
+
+// One vector alone is sketched by the grid-wide kernels (K2: weight sample,
+// filter, list walk, heavy walk -- every SM) once it has this many elements;
+// below it the batched kernel's single CTA is faster (GM_SINGLE_GRID_MIN
+// overrides; 0 disables).  Results are identical (ids are distinct within a
+// vector, so K2's duplicate rule never applies).
+static int64_t single_vector_grid_min() {
+  static const int64_t v = getenv("GM_SINGLE_GRID_MIN") ? atoll(getenv("GM_SINGLE_GRID_MIN")) : 4096;
+  return v > 0 ? v : INT64_MAX;
+}
+
+static int single_vector_grid(const void* ids, int id_bits, const void* w, int w_bits, int64_t n, int32_t k,
+                              uint64_t seed, uint64_t salt, uint32_t flags, double* y_out, uint64_t* s_out,
+                              int64_t* emitted_out, Workspace* ws, cudaStream_t st) {
+  const size_t ib = (size_t)n * (id_bits / 8), wb = (size_t)n * (w_bits / 8), yb = (size_t)k * 8;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const bool s32 = flags & GM_FLAG_S32;
+  int rc = grow((unsigned char**)&ws->stage, &ws->stage_cap, al(ib) + al(wb) + 2 * al(yb) + al(yb / 2), st);
   if (rc) return rc;
-  if (n_vec < 0) return fail(GM_ERR_INVALID_PARAMETER, "n_vec must be >= 0");
-  if (n_vec == 0) return GM_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  Workspace* ws = nullptr;
-  rc = get_ws(st, &ws);
+  unsigned char* base = (unsigned char*)ws->stage;
+  void* d_ids = base;
+  void* d_w = base + al(ib);
+  double* d_y = (double*)(base + al(ib) + al(wb));
+  u64* d_s = (u64*)((unsigned char*)d_y + al(yb));
+  u32* d_s32 = (u32*)((unsigned char*)d_s + al(yb));
+  CK(cudaMemcpyAsync(d_ids, ids, ib, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_w, w, wb, cudaMemcpyHostToDevice, st));
+  rc = gm_sketch_elements(d_ids, id_bits, d_w, w_bits, n, k, seed, salt, flags & GM_FLAG_EXHAUSTIVE, d_y, d_s,
+                          emitted_out, st);
   if (rc) return rc;
-  const u64 useed = global_seed;
-  const u64 pseed = global_seed ^ stream_salt;
-  const u32 kk = (u32)k;
-  const bool small_k = kk <= 512;  // CsrSmallK: four vector slots
-  // exhaustive = a single pass with tau = +inf (pass_tau's last attempt)
-  const int a0 = (flags & GM_FLAG_EXHAUSTIVE) ? 3 : 0;
-  if (id_bits == 32 && w_bits == 32)
-    rc = small_k ? launch_csr<CsrSmallK, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0)
-                 : launch_csr<CsrDefault, u32, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
-  else if (id_bits == 32)
-    rc = small_k ? launch_csr<CsrSmallK, u32, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0)
-                 : launch_csr<CsrDefault, u32, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
-  else if (w_bits == 32)
-    rc = small_k ? launch_csr<CsrSmallK, u64, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0)
-                 : launch_csr<CsrDefault, u64, float>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
-  else
-    rc = small_k ? launch_csr<CsrSmallK, u64, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0)
-                 : launch_csr<CsrDefault, u64, double>(ids, w, offsets, n_vec, kk, useed, pseed, y_out, s_out, emitted_out, ws, st, a0);
-  if (rc == -1) return csr_by_elements(ids, id_bits, w, w_bits, offsets, n_vec, k, global_seed,
-                                       stream_salt, flags, y_out, s_out, emitted_out, st);
-  if (rc) return rc;
-  if (flags & GM_FLAG_ASYNC) return GM_OK;
-  return check_sync(ws, st);
+  CK(cudaMemcpyAsync(y_out, d_y, yb, cudaMemcpyDeviceToHost, st));
+  if (s32) {
+    narrow_u32_kernel<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(d_s, d_s32, k);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(s_out, d_s32, yb / 2, cudaMemcpyDeviceToHost, st));
+  } else {
+    CK(cudaMemcpyAsync(s_out, d_s, yb, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return GM_OK;
 }
 
 // device address of a page-locked host buffer (nullptr if the buffer is
@@ -687,6 +839,9 @@ int gm_sketch_csr_host(const void* ids, int id_bits, const void* w, int w_bits,
   const bool s32 = flags & GM_FLAG_S32;
   if (s32 && id_bits != 32) return fail(GM_ERR_INVALID_PARAMETER, "GM_FLAG_S32 needs 32-bit ids");
   const int64_t n = offsets[n_vec];
+  if (n_vec == 1 && !(flags & GM_FLAG_ASYNC) && offsets[0] == 0 && n >= single_vector_grid_min())
+    return single_vector_grid(ids, id_bits, w, w_bits, n, k, global_seed, stream_salt, flags, y_out, s_out,
+                              emitted_out, ws, st);
   const size_t ib = (size_t)n * (id_bits / 8), wb = (size_t)n * (w_bits / 8);
   const size_t ob = (size_t)(n_vec + 1) * 8, yb = (size_t)n_vec * k * 8;
   // results go straight to page-locked host buffers (the kernel's stores
@@ -930,12 +1085,19 @@ int gm_log_batch(const double* x, int64_t n, double* out, void* stream) {
 }
 
 int gm_probe_arrival_rate(int64_t n_threads, int32_t iters, int32_t k, double* sink, void* stream) {
+  // n_threads threads, each walking `chains` element queues (chains = 1, 2
+  // or 4 from the high bits of iters: iters | chains << 24) for `iters` arrivals
   g_msg[0] = 0;
   (void)cudaGetLastError();
-  if (k < 2 || k > 65536 || iters < 1 || n_threads < NT)
+  const int chains = (iters >> 24) ? (iters >> 24) : 2;
+  iters &= 0xFFFFFF;
+  if (k < 128 || k > 65536 || iters < 1 || n_threads < NT || (chains != 1 && chains != 2 && chains != 4))
     return fail(GM_ERR_INVALID_PARAMETER, "bad probe arguments");
-  arrival_probe_kernel<<<(unsigned)(n_threads / NT), NT, 0, (cudaStream_t)stream>>>(
-      iters, (u32)k, 0x1234ull, 0x5678ull, sink);
+  const unsigned grid = (unsigned)(n_threads / NT);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (chains == 1) arrival_probe_kernel<1><<<grid, NT, 0, st>>>(iters, (u32)k, 0x1234ull, 0x5678ull, sink);
+  else if (chains == 2) arrival_probe_kernel<2><<<grid, NT, 0, st>>>(iters, (u32)k, 0x1234ull, 0x5678ull, sink);
+  else arrival_probe_kernel<4><<<grid, NT, 0, st>>>(iters, (u32)k, 0x1234ull, 0x5678ull, sink);
   CK(cudaGetLastError());
   return GM_OK;
 }

@@ -67,6 +67,7 @@ struct SlotInfo {
   unsigned long long emitted;
   unsigned long long grab;  // (n << 32) | next element index: a ticket and the
                             // element count it is valid for come from one atomic
+  u64 useed, pseed;         // the vector's uniform / permutation stream seeds
   int n;                   // elements
   int done;                // completed elements of this pass
   int attempt;
@@ -283,7 +284,7 @@ template <class C, class WT>
 __device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const int64_t* offsets,
                           int64_t n_vec, const double* Wsum, const int* vflags, int* vec_counter,
                           unsigned long long* err, int attempt0, int lane, const int* vec_list,
-                          const WT* wts) {
+                          const WT* wts, u64 useed, u64 salt, const u64* vseeds, int one_vec) {
   const unsigned FULL = 0xFFFFFFFFu;
   SlotInfo& sl = S.slot[s];
   for (;;) {
@@ -300,7 +301,10 @@ __device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const
       return;
     }
     if (vec_list) v = vec_list[v];  // a subset of the batch (re-runs)
-    const int64_t lo = offsets[v], n = offsets[v + 1] - lo;
+    // one_vec: every sketch of the batch is of the single vector offsets[0..1]
+    // (one vector under many seeds, gm_sketch_csr_seeded + GM_FLAG_ONE_VECTOR)
+    const int64_t* ov = one_vec ? offsets : offsets + v;
+    const int64_t lo = ov[0], n = ov[1] - lo;
     if (n <= 0) {  // EmptyVectorError (latched here without a prep kernel)
       if (!Wsum && lane == 0) atomicCAS(err, 0ull, ((unsigned long long)(v & 0xFFFFFFFF) << 32) | 1u);
       continue;
@@ -345,6 +349,9 @@ __device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const
       sl.lo = lo;
       sl.n = (int)n;
       sl.W = Wsum ? Wsum[v] : W;
+      // per-vector seeds (a batch of one vector under many seeds) or the batch's
+      sl.useed = vseeds ? vseeds[v] : useed;
+      sl.pseed = sl.useed ^ salt;
       sl.fast = Wsum ? (vflags[v] & 1) : fast;
       sl.emitted = 0;
       sl.seq = ++S.seq;
@@ -357,44 +364,14 @@ __device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const
   }
 }
 
-// ---- prep kernel: per-vector total weight, validation, divide range -------
-template <class WT>
-__global__ void __launch_bounds__(256) csr_prep_kernel(const WT* __restrict__ wts, const int64_t* __restrict__ offsets,
-                                                       int64_t n_vec, double* __restrict__ Wsum,
-                                                       int* __restrict__ vflags, unsigned long long* err) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t v = gw; v < n_vec; v += nw) {
-    const int64_t lo = offsets[v], hi = offsets[v + 1];
-    double ws = 0.0;
-    int fast = 1, bad = 0;
-    for (int64_t i = lo + lane; i < hi; i += 32) {
-      const double w = (double)__ldg(&wts[i]);
-      bad |= !(isfinite(w) && w > 0.0 && w >= 1e-300);
-      fast &= w_fast(w);
-      ws += w;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) ws += __shfl_xor_sync(0xFFFFFFFFu, ws, o);
-    fast = __all_sync(0xFFFFFFFFu, fast);
-    bad = __any_sync(0xFFFFFFFFu, bad);
-    if (lane == 0) {
-      Wsum[v] = ws;
-      vflags[v] = fast;
-      if (hi <= lo) atomicCAS(err, 0ull, ((unsigned long long)(v & 0xFFFFFFFF) << 32) | 1u);
-      else if (bad) atomicCAS(err, 0ull, ((unsigned long long)(v & 0xFFFFFFFF) << 32) | 2u);
-    }
-  }
-}
-
 // ---- K1 ---------------------------------------------------------------------
 // Dynamic shared memory: Reg regs[V][k] | u32 tables[NB][NT][4] | u32 mtab[MTAB]
 //   | double scan[NWARP][32] | int prov[NWARP][32]
 template <class C, class IdT, class WT>
 __global__ void __launch_bounds__(C::NT, C::MINB)
     csr3_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts,
-                const int64_t* __restrict__ offsets, int64_t n_vec, u32 k, u64 useed, u64 pseed,
+                const int64_t* __restrict__ offsets, int64_t n_vec, u32 k, u64 useed, u64 salt,
+                const u64* __restrict__ vseeds, int one_vec,
                 const double* __restrict__ Wsum, const int* __restrict__ vflags,
                 double* __restrict__ y_out, u64* __restrict__ s_out,
                 int64_t* __restrict__ emitted_out, int* __restrict__ vec_counter,
@@ -434,7 +411,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   __syncthreads();
   if (warp < V)
     slot_load<C, WT>(S, warp, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list,
-                     wts);
+                     wts, useed, salt, vseeds, one_vec);
   __syncthreads();
 
   Lane L;
@@ -516,7 +493,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
                  ((unsigned long long)blockIdx.x << 48) | ((unsigned long long)s << 60));
       __syncwarp();
       slot_load<C, WT>(S, s, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list,
-                       wts);
+                       wts, useed, salt, vseeds, one_vec);
     }
 
 #ifdef GM_STATS
@@ -536,6 +513,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       const double b0 = wres ? __shfl_sync(FULL, L.b, src) : 0.0;
       const bool wfast = __shfl_sync(FULL, (int)L.fast, src) != 0;
       const u32 em0 = __shfl_sync(FULL, em, src);
+      const u64 wus = *(volatile u64*)&S.slot[s].useed, wps = *(volatile u64*)&S.slot[s].pseed;
       if (++stamp > 0xFFFFu) {
         for (u32 i = lane; i < k; i += 32) dense[i] = 0;
         __syncwarp();
@@ -552,10 +530,10 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       u32 wem = 0;
       Reg* regs = slot_regs<C>(smem_raw, s, k);
       if (wfast)
-        walk_warp<true, true>(wid, ww, tau, k, useed, pseed, dense, stamp, scan, prov, regs, nullptr, wem, z0, b0,
+        walk_warp<true, true>(wid, ww, tau, k, wus, wps, dense, stamp, scan, prov, regs, nullptr, wem, z0, b0,
                               mtab, (u32)C::MTAB);
       else
-        walk_warp<true, false>(wid, ww, tau, k, useed, pseed, dense, stamp, scan, prov, regs, nullptr, wem, z0, b0,
+        walk_warp<true, false>(wid, ww, tau, k, wus, wps, dense, stamp, scan, prov, regs, nullptr, wem, z0, b0,
                                mtab, (u32)C::MTAB);
       wem = __shfl_sync(FULL, wem, 0);
       GM_STAT(3, lane == 0);  // warp walks
@@ -661,8 +639,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
           L.tau = sl.tau;
           L.fast = sl.fast != 0;
           L.regs = slot_regs<C>(smem_raw, ps, k);
-          L.ubase = useed + pid * K_ELEM;
-          L.pbase = pseed + pid * K_ELEM;
+          L.ubase = sl.useed + pid * K_ELEM;
+          L.pbase = sl.pseed + pid * K_ELEM;
           L.b = 0.0;
           L.z = 0;
           L.used = 0;

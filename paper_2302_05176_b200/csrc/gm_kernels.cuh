@@ -903,23 +903,49 @@ __global__ void log_batch_kernel(const double* x, int64_t n, double* out) {
 }
 
 // ---- diagnostics ----
-// Speed-of-light probe for the arrival generator: every thread emits a
-// long run of exact arrivals (spacing + permutation draw) with no pruning,
-// no registers, no divergence and no memory traffic.  Its rate is the
-// compute roofline the sketch kernels are reported against.
-__global__ void __launch_bounds__(NT) arrival_probe_kernel(int iters, u32 k, u64 useed, u64 pseed,
-                                                           double* sink) {
-  const u64 id = (u64)blockIdx.x * NT + threadIdx.x;
-  const u64 ubase = useed + id * K_ELEM, pbase = pseed + id * K_ELEM;
-  double b = 0.0;
+// Speed-of-light probe for the arrival generator (the roofline K1 is
+// reported against): every thread walks C independent element queues with
+// exactly the lane step's arithmetic per arrival -- the uniform hash,
+// u_open, the glibc-clone log with the table in shared memory, the rounded
+// product w (k - z + 1), the branch-free divide, the prefix add, and the
+// permutation hash with the 64-bit Barrett reduction from a shared-memory
+// table -- with no pruning, no Fisher-Yates table, no register update, no
+// queue bookkeeping and no memory traffic.  C chains per thread give the
+// scheduler independent work (ILP) on top of full occupancy.
+template <int C>
+__global__ void __launch_bounds__(NT) arrival_probe_kernel(int iters, u32 k, u64 useed, u64 pseed, double* sink) {
+  __shared__ __align__(16) double ltab[256];
+  __shared__ u64 mtab64[128];
+  for (u32 i = threadIdx.x; i < 256; i += NT) ltab[i] = gm_glog_tab[i >> 1][i & 1];
+  for (u32 z = threadIdx.x; z < 128; z += NT) mtab64[z] = barrett_magic64(k - z + 1);
+  __syncthreads();
+  u64 ub[C], pb[C];
+  double b[C], w[C];
   u32 acc = 0;
-  const double w = 1.0 + (double)(threadIdx.x & 7);
-  for (int i = 0; i < iters; ++i) {
-    const u32 z = 1u + ((u32)i % (k - 1u));
-    b = __dadd_rn(b, spacing(ubase, z, w, k));
-    acc += perm_draw(pbase, z, k);
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const u64 id = ((u64)blockIdx.x * NT + threadIdx.x) * C + c;
+    ub[c] = useed + id * K_ELEM;
+    pb[c] = pseed + id * K_ELEM;
+    b[c] = 0.0;
+    w[c] = 1.0 + (double)((threadIdx.x + c) & 7);
   }
-  if (b == -1.0 || acc == 0xFFFFFFFFu) sink[0] = b + (double)acc;
+  for (int i = 0; i < iters; ++i) {
+    const u32 z = 1u + ((u32)i & 126u);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const u64 x = mix64(ub[c] + (u64)z * K_STEP);
+      const double L = -log_pos_t(u_open(x), ltab);
+      const double D = __dmul_rn(w[c], (double)(k - z + 1));
+      b[c] = __dadd_rn(b[c], ddiv_fast(L, D));
+      const u64 g = mix64(pb[c] + (u64)z * K_STEP);
+      acc += z + mod_barrett64(g, k - z + 1, mtab64[z]);
+    }
+  }
+  double t = 0.0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) t += b[c];
+  if (t == -1.0 || acc == 0xFFFFFFFFu) sink[0] = t + (double)acc;
 }
 
 // Number of arrivals t <= tau_v of every element of every CSR vector

@@ -1,24 +1,31 @@
-"""Multi-GPU partitioning (one process per GPU, torch.distributed plumbing).
+"""Multi-GPU partitioning (one process per GPU; torch.distributed only for
+the rendezvous, the register exchange is NCCL inside the C ABI).
 
 Two shapes, SURVEY.md section 8(e):
   * a batch of independent vectors (configs 2-3): contiguous vector ranges
     balanced by element count; no data-path collective.
   * one huge vector or stream (configs 4-5): contiguous element ranges, a
-    sketch per rank, then ONE exchange: every rank all-gathers the k
-    registers (k x 16 B) and min-merges them in rank order with the device
-    merge kernel, which reproduces merge([sketch_rank0, sketch_rank1, ...])
-    exactly (estimate.py:103-125; partition law test_estimate.py:174-199).
-    `allreduce_min_registers` is the collective-only alternative: two
-    all-reduces with MIN (y, then the ids of the registers that hold the
-    minimum), the register-wise lexicographic (y, id) minimum -- the whole
-    element set's sketch (sketch_naive's smaller-id tie rule, sketch.py:196-205).
+    sketch per rank, then ONE exchange of the k registers (k x 16 B) over
+    NCCL, in place on every rank (RegisterExchange; gm_comm.cuh):
+      - allreduce_min: two all-reduces with MIN (y, then the ids of the
+        ranks holding the minimum) -- the register-wise lexicographic (y, id)
+        minimum, sketch_naive's smaller-id tie rule (sketch.py:196-205);
+      - allgather_merge: all-gather + the device merge in rank order --
+        merge([sketch_rank0, sketch_rank1, ...]) exactly (estimate.py:103-125).
+    Both reproduce the whole set's sketch (partition law,
+    test_estimate.py:174-199; the reference's "sketch per site, merge
+    centrally").
 """
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 import torch.distributed as dist
+
+from . import _device, _lib
 
 
 def element_range(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -44,39 +51,43 @@ def vector_ranges(offsets, world: int) -> list[tuple[int, int]]:
     return [(cuts[r], cuts[r + 1]) for r in range(world)]
 
 
-def gather_registers(y: torch.Tensor, s: torch.Tensor, group=None) -> tuple[torch.Tensor, torch.Tensor]:
-    """All-gather one sketch's registers from every rank: ([world, k], [world, k])."""
-    world = dist.get_world_size(group)
-    ys = [torch.empty_like(y) for _ in range(world)]
-    ss = [torch.empty_like(s) for _ in range(world)]
-    dist.all_gather(ys, y.contiguous(), group=group)
-    dist.all_gather(ss, s.contiguous(), group=group)
-    return torch.stack(ys), torch.stack(ss)
+class RegisterExchange:
+    """An NCCL communicator owned by the C ABI (gm_comm_init) for the ranks
+    of `group`; torch.distributed carries only its unique id from rank 0.
+    Exchanges run in place on (y float64 [k], s int64 [k] holding uint64
+    ids) device tensors, on the current CUDA stream."""
 
+    def __init__(self, group=None):
+        L = _lib.load()
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        nbytes = L.gm_comm_id_bytes()
+        uid = (ctypes.c_char * nbytes)()
+        if self.rank == 0:
+            _device.call("gm_comm_unique_id", ctypes.addressof(uid))
+        box = [bytes(uid) if self.rank == 0 else None]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        uid = (ctypes.c_char * nbytes).from_buffer_copy(box[0])
+        self._comm = ctypes.c_void_p()
+        _device.call("gm_comm_init", ctypes.addressof(uid), self.world, self.rank, ctypes.byref(self._comm))
 
-def merge_across_ranks(y: torch.Tensor, s: torch.Tensor, group=None) -> tuple[torch.Tensor, torch.Tensor]:
-    """Exchange + device min-merge: every rank ends with the merged sketch."""
-    from .estimate import merge_arrays
+    def allreduce_min(self, y: torch.Tensor, s: torch.Tensor):
+        _device.call("gm_allreduce_min_registers", self._comm, y.data_ptr(), s.data_ptr(), y.numel(),
+                     _device.stream_ptr())
+        return y, s
 
-    ya, sa = gather_registers(y, s, group)
-    return merge_arrays(ya, sa)
+    def allgather_merge(self, y: torch.Tensor, s: torch.Tensor):
+        _device.call("gm_allgather_merge_registers", self._comm, y.data_ptr(), s.data_ptr(), y.numel(),
+                     _device.stream_ptr())
+        return y, s
 
+    def close(self) -> None:
+        if self._comm:
+            _device.call("gm_comm_destroy", self._comm)
+            self._comm = ctypes.c_void_p()
 
-_SIGN = 1 << 63
+    def __enter__(self):
+        return self
 
-
-def allreduce_min_registers(y: torch.Tensor, s: torch.Tensor, group=None) -> tuple[torch.Tensor, torch.Tensor]:
-    """Every rank ends with the register-wise lexicographic minimum of
-    (y, s) over the ranks: all-reduce(MIN) of y, then all-reduce(MIN) of the
-    ids of the ranks that hold that minimum (others contribute the largest
-    id).  Ids are unsigned 64-bit values carried in int64: the sign bit is
-    flipped so that signed MIN orders them as unsigned.  Equal to the
-    rank-order merge unless two ranks hold different elements with the very
-    same y bits in one register (then the smaller id wins, as in
-    sketch_naive over the whole set)."""
-    ym = y.clone()
-    dist.all_reduce(ym, op=dist.ReduceOp.MIN, group=group)
-    sign = torch.tensor(-_SIGN, dtype=torch.int64, device=s.device)  # bit pattern 1 << 63
-    key = torch.where(y == ym, s ^ sign, torch.full_like(s, (1 << 63) - 1))
-    dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)
-    return ym, key ^ sign
+    def __exit__(self, *exc):
+        self.close()

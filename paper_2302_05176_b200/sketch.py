@@ -179,8 +179,9 @@ class SketchBatch:
     k: int
     y: torch.Tensor
     s: torch.Tensor
-    fingerprint: int
+    fingerprint: int | None
     emitted: torch.Tensor | None = None
+    fingerprints: list[int] | None = None  # per sketch (sketch_csr_seeded), else None
 
     def __len__(self) -> int:
         return self.y.shape[0]
@@ -188,8 +189,9 @@ class SketchBatch:
     def to_sketches(self) -> list[GumbelMaxSketch]:
         y = self.y.cpu().numpy()
         s = self.s.cpu().numpy().view(np.uint64)
+        fps = self.fingerprints or [self.fingerprint] * y.shape[0]
         return [GumbelMaxSketch(self.k, tuple(int(x) for x in s[i]), tuple(y[i].tolist()),
-                                self.fingerprint) for i in range(y.shape[0])]
+                                fps[i]) for i in range(y.shape[0])]
 
 
 def _check_k(k: int) -> None:
@@ -232,6 +234,50 @@ def sketch_csr(ids, weights, offsets, k: int, scheme: SeedScheme, *, exhaustive:
         exact_y_host(ids_t.cpu(), w_t.cpu(), off_t.cpu(), k, scheme, s.cpu(), y_h)
         y.copy_(y_h)
     return SketchBatch(k, y, s, scheme.fingerprint, em)
+
+
+def sketch_vector_seeds(ids, weights, k: int, schemes: Sequence[SeedScheme], *, exhaustive: bool = False,
+                        counted: bool = False) -> SketchBatch:
+    """R sketches of ONE vector, one per SeedScheme, in one launch
+    (gm_sketch_csr_seeded + GM_FLAG_ONE_VECTOR: the vector is stored once).
+    Row r equals sketch_csr of the vector under schemes[r]."""
+    n = len(ids)
+    return sketch_csr_seeded(ids, weights, np.array([0, n], np.int64), k, schemes, exhaustive=exhaustive,
+                             counted=counted, one_vector=True)
+
+
+def sketch_csr_seeded(ids, weights, offsets, k: int, schemes: Sequence[SeedScheme], *,
+                      exhaustive: bool = False, counted: bool = False, one_vector: bool = False) -> SketchBatch:
+    """sketch_csr with one SeedScheme per vector (gm_sketch_csr_seeded).  All
+    schemes must share the stream salt (the permutation seed is
+    global_seed ^ salt, randgen.py:72-95).  ``one_vector``: offsets is
+    [lo, hi] of a single vector and len(schemes) sketches of it are made."""
+    _check_k(k)
+    dev = _device.require_cuda()
+    salts = {sc.stream_salt for sc in schemes}
+    if len(salts) != 1:
+        raise InvalidParameterError("sketch_csr_seeded: every scheme must have the same stream salt")
+    ids_t = ids if isinstance(ids, torch.Tensor) else torch.from_numpy(_as_id_np(ids))
+    w_t = weights if isinstance(weights, torch.Tensor) else torch.from_numpy(_device.weight_array(weights)[0])
+    off_t = offsets if isinstance(offsets, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(offsets, dtype=np.int64)))
+    ids_t, w_t = ids_t.to(dev).contiguous(), w_t.to(dev).contiguous()
+    off_t = off_t.to(dev, dtype=torch.int64).contiguous()
+    n_vec = len(schemes) if one_vector else off_t.numel() - 1
+    if one_vector and off_t.numel() != 2:
+        raise InvalidParameterError("one_vector: offsets must be [lo, hi]")
+    if len(schemes) != n_vec:
+        raise InvalidParameterError(f"{len(schemes)} schemes for {n_vec} vectors")
+    seeds = torch.from_numpy(np.array([sc.global_seed for sc in schemes], dtype=np.uint64).view(np.int64)).to(dev)
+    y = torch.empty((n_vec, k), dtype=torch.float64, device=dev)
+    s = torch.empty((n_vec, k), dtype=torch.int64, device=dev)
+    em = torch.empty(n_vec, dtype=torch.int64, device=dev) if counted else None
+    _device.call("gm_sketch_csr_seeded", ids_t.data_ptr(), _device.id_bits_of(ids_t), w_t.data_ptr(),
+                 _device.w_bits_of(w_t), off_t.data_ptr(), n_vec, k, seeds.data_ptr(), salts.pop(),
+                 (_lib.GM_FLAG_EXHAUSTIVE if exhaustive else 0) | (_lib.GM_FLAG_ONE_VECTOR if one_vector else 0),
+                 y.data_ptr(), s.data_ptr(), _device.ptr(em),
+                 _device.stream_ptr())
+    return SketchBatch(k, y, s, None, em, [sc.fingerprint for sc in schemes])
 
 
 def sketch_csr_host(ids, weights, offsets, k: int, scheme: SeedScheme, *, out=None,

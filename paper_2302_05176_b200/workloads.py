@@ -11,6 +11,9 @@ deterministic, return host arrays in the device layouts the C-ABI takes
 
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 K_ELEM = 0x9E3779B97F4A7C15
@@ -86,33 +89,79 @@ def config3(n_vectors: int = 100_000):
     return ids.astype(np.uint32), w, offsets, 512, 1
 
 
-def config4(n_pairs: int = 10**8, n_keys: int = 10**7):
-    """Config 4: weighted-cardinality stream of (u64 id, f32 weight) pairs.
-    10**7 key weights fp32 U(0.1, 10); ranks ~ Zipf(1.1) truncated to
-    <= n_keys by rejection; id = mix64(rank); stream order = draw order;
-    k=4096; seed 1.  Returns (ids u64, w f32, k, seed)."""
-    rng = np.random.default_rng(4)
-    key_w = rng.uniform(0.1, 10.0, size=n_keys).astype(np.float32)
-    ranks = np.empty(n_pairs, dtype=np.int64)
+def _parallel(fn, items) -> None:
+    items = list(items)
+    if len(items) <= 1:
+        for c in items:
+            fn(c)
+        return
+    with ThreadPoolExecutor(min(len(items), os.cpu_count() or 1)) as ex:
+        list(ex.map(fn, items))
+
+
+PAIR_CHUNK = 1 << 22   # config 4: pairs per keyed chunk
+ELEM_CHUNK = 1 << 26   # config 5: elements per keyed chunk
+
+
+def _config4_chunk(c: int, size: int, n_keys: int) -> np.ndarray:
+    """Zipf(1.1) ranks <= n_keys (truncated by rejection) of pair chunk c,
+    from its own generator default_rng([4, c]): any range of the stream can
+    be generated alone (a rank of an N-GPU job makes only its shard)."""
+    rng = np.random.default_rng([4, c])
+    out = np.empty(size, dtype=np.int64)
     filled = 0
-    while filled < n_pairs:
-        need = n_pairs - filled
+    while filled < size:
+        need = size - filled
         draw = rng.zipf(1.1, size=int(need * 1.45) + 1024)
         draw = draw[draw <= n_keys][:need]
-        ranks[filled:filled + draw.size] = draw
+        out[filled:filled + draw.size] = draw
         filled += draw.size
+    return out
+
+
+def config4(n_pairs: int = 10**8, n_keys: int = 10**7, lo: int = 0, hi: int | None = None):
+    """Config 4: weighted-cardinality stream of (u64 id, f32 weight) pairs.
+    10**7 key weights fp32 U(0.1, 10) (default_rng(4)); ranks ~ Zipf(1.1)
+    truncated to <= n_keys by rejection, drawn in keyed chunks of PAIR_CHUNK
+    pairs (default_rng([4, chunk])); id = mix64(rank); stream order = draw
+    order; k=4096; seed 1.  ``lo:hi`` selects a contiguous range of the
+    stream (generated alone).  Returns (ids u64, w f32, k, seed)."""
+    hi = n_pairs if hi is None else min(hi, n_pairs)
+    lo = max(0, min(lo, hi))
+    key_w = np.random.default_rng(4).uniform(0.1, 10.0, size=n_keys).astype(np.float32)
+    ranks = np.empty(hi - lo, dtype=np.int64)
+
+    def fill(c):  # chunks are independent: generated on all host threads
+        c0 = c * PAIR_CHUNK
+        c1 = min(c0 + PAIR_CHUNK, n_pairs)
+        r = _config4_chunk(c, c1 - c0, n_keys)
+        a, b = max(lo, c0), min(hi, c1)
+        ranks[a - lo:b - lo] = r[a - c0:b - c0]
+
+    _parallel(fill, range(lo // PAIR_CHUNK, (hi + PAIR_CHUNK - 1) // PAIR_CHUNK))
     ids = mix64_np(ranks.astype(np.uint64))
     return ids, key_w[ranks - 1], 4096, 1
 
 
-def config5(n: int = 10**9, chunk: int = 1 << 26):
+def config5(n: int = 10**9, lo: int = 0, hi: int | None = None):
     """Config 5: one huge vector, ids 0..n-1 (u32), weights fp32
-    LogNormal(0, 2) from default_rng(5) generated in chunks; k=8192; seed 1.
-    Returns (ids u32, w f32, k, seed)."""
-    rng = np.random.default_rng(5)
-    w = np.empty(n, dtype=np.float32)
-    for lo in range(0, n, chunk):
-        hi = min(n, lo + chunk)
-        w[lo:hi] = rng.lognormal(0.0, 2.0, hi - lo)
-    ids = np.arange(n, dtype=np.uint32)
+    LogNormal(0, 2), drawn in keyed chunks of ELEM_CHUNK elements
+    (default_rng([5, chunk])); k=8192; seed 1.  ``lo:hi`` selects a
+    contiguous element range (generated alone).  Returns (ids u32, w f32,
+    k, seed)."""
+    hi = n if hi is None else min(hi, n)
+    lo = max(0, min(lo, hi))
+    w = np.empty(hi - lo, dtype=np.float32)
+
+    def fill(c):
+        c0 = c * ELEM_CHUNK
+        c1 = min(c0 + ELEM_CHUNK, n)
+        a, b = max(lo, c0), min(hi, c1)
+        rng = np.random.default_rng([5, c])
+        if a > c0:
+            rng.lognormal(0.0, 2.0, a - c0)  # advance to a (same stream as the whole chunk)
+        w[a - lo:b - lo] = rng.lognormal(0.0, 2.0, b - a)
+
+    _parallel(fill, range(lo // ELEM_CHUNK, (hi + ELEM_CHUNK - 1) // ELEM_CHUNK))
+    ids = np.arange(lo, hi, dtype=np.uint32)
     return ids, w, 8192, 1

@@ -217,6 +217,7 @@ def test_config2_full_vs_oracle():
     rc, yo, so, _ = O.sketch_csr(ids.astype(np.uint64), w.astype(np.float64), off, k, seed, mode=0, threads=8)
     assert rc == 0
     assert_regs(y, s, yo, so)
+    assert O.digest(y, s) == load_json("full_digests.json")["config2"]["digest"]
     # estimator batch: matches of pairs (2i, 2i+1)
     sa = torch.from_numpy(s[0::2].view(np.int64)).cuda()
     sb = torch.from_numpy(s[1::2].view(np.int64)).cuda()
@@ -243,6 +244,7 @@ def test_config3_full_vs_oracle():
                                  threads=os.cpu_count() or 8)
     assert rc == 0
     assert_regs(y, s, yo, so)
+    assert O.digest(y, s) == load_json("full_digests.json")["config3"]["digest"]
 
 
 def test_config4_prefix_vs_oracle():
@@ -288,6 +290,74 @@ def test_config5_prefix_vs_oracle():
     rc, yo, so, _, _ = O.sketch_stream(ids.astype(np.uint64), w.astype(np.float64), 8192, 1)
     assert rc == 0
     assert_regs(y.cpu().numpy(), s.cpu().numpy().view(np.uint64), yo, so)
+
+
+def _full_elements_vs_oracle(cfg):
+    ids, w, k, seed = workloads.config4() if cfg == 4 else workloads.config5()
+    y, s, _ = gm.sketch_elements(ids, w, k, gm.SeedScheme(seed))
+    y, s = y.cpu().numpy(), s.cpu().numpy().view(np.uint64)
+    rc, yo, so = O.sketch_stream_chunked(ids, w, k, seed)
+    assert rc == 0
+    assert_regs(y, s, yo, so)
+    assert y.tobytes() == yo.tobytes()
+    want = load_json("full_digests.json")[f"config{cfg}"]["digest"]
+    assert O.digest(yo, so) == want and O.digest(y, s) == want
+
+
+def test_config4_full_vs_oracle():
+    """All of config 4 (1e8 Zipf stream pairs, k=4096) against the oracle's
+    sketch_stream run in contiguous chunks on all host threads and merged by
+    the partition law, and against the committed oracle digest."""
+    _full_elements_vs_oracle(4)
+
+
+def test_config5_full_vs_oracle():
+    """All of config 5 (1e9 elements, k=8192), as test_config4_full_vs_oracle."""
+    _full_elements_vs_oracle(5)
+
+
+def test_seeded_batch_one_vector_many_seeds():
+    """Config 1's vector under R seeds in one launch (gm_sketch_csr_seeded)
+    equals R separate sketches, and the oracle for a few of them."""
+    ids, w, k, seed = workloads.config1()
+    R = 40
+    schemes = [gm.SeedScheme(1000 + r) for r in range(R)]
+    off = np.arange(R + 1, dtype=np.int64) * ids.size
+    b = gm.sketch_csr_seeded(np.tile(ids, R), np.tile(w, R), off, k, schemes)
+    y, s = batch_np(b)
+    for r in (0, 7, R - 1):
+        y1, s1 = batch_np(gm.sketch_csr(ids, w, np.array([0, ids.size]), k, schemes[r]))
+        assert y1.tobytes() == y[r:r + 1].tobytes() and np.array_equal(s1[0], s[r])
+        rc, yo, so, _, _ = O.sketch_stream(ids.astype(np.uint64), w, k, 1000 + r)
+        assert rc == 0
+        assert_regs(y[r], s[r], yo, so)
+    sks = b.to_sketches()
+    assert [sk.fingerprint for sk in sks] == [sc.fingerprint for sc in schemes]
+    # the vector stored once (GM_FLAG_ONE_VECTOR): the same R sketches
+    b1 = gm.sketch_vector_seeds(ids, w, k, schemes)
+    assert torch.equal(b1.y, b.y) and torch.equal(b1.s, b.s)
+
+
+@pytest.mark.parametrize("n", [4096, 10_000, 300_000])
+def test_single_vector_runs_grid_wide(n):
+    """One vector of >= 4096 elements through the host entry (sketch_fast,
+    sketch_csr_host) runs on the grid-wide kernels; the registers are the
+    oracle's and the batched single-CTA kernel's."""
+    rng = np.random.default_rng(n)
+    ids = rng.choice(1 << 31, n, replace=False).astype(np.uint32) + 1
+    w = rng.exponential(1.0, n) + 1e-3
+    k = 256 if n < 100_000 else 2048
+    sc = gm.SeedScheme(n)
+    yh, sh, em = gm.sketch_csr_host(ids, w, np.array([0, n]), k, sc, counted=True)
+    yd, sd = batch_np(gm.sketch_csr(ids, w, np.array([0, n]), k, sc))
+    assert yh.tobytes() == yd.tobytes() and np.array_equal(sh, sd)
+    order = np.argsort(ids)
+    rc, yo, so, _ = O.sketch_fast(ids[order].astype(np.uint64), w[order], k, n)
+    assert rc == 0
+    assert_regs(yh[0], sh[0], yo, so)
+    v = gm.WeightedVector(dict(zip(ids.tolist(), w.tolist())))
+    sk = gm.sketch_fast(v, gm.GenerationParams(k=k, scheme=sc))
+    assert list(sk.y) == yo.tolist() and np.array_equal(np.array(sk.s, np.uint64), so)
 
 
 # ---------------------------------------------------------------- size-independent properties at full size
@@ -602,6 +672,60 @@ def test_accumulate_light_then_heavy_flush(seed):
     gm.sketch_elements(heavy, wh, 64, gm.SeedScheme(seed), into=(y, s))
     rc, yo, so, _, _ = O.sketch_stream(ids, w, 64, seed)
     assert_regs(y.cpu().numpy(), s.cpu().numpy().view(np.uint64), yo, so)
+
+
+def test_nccl_exchange_world1():
+    """The C ABI's NCCL register exchange (gm_comm.cuh) on one rank: both
+    protocols leave a sketch unchanged; the communicator is created and
+    destroyed through the C ABI (the N > 1 protocol is covered on CPU by
+    tests/test_multirank_gloo.py)."""
+    import ctypes
+    from paper_2302_05176_b200 import _device, _lib
+    L = _lib.load()
+    uid = (ctypes.c_char * L.gm_comm_id_bytes())()
+    _device.call("gm_comm_unique_id", ctypes.addressof(uid))
+    comm = ctypes.c_void_p()
+    _device.call("gm_comm_init", ctypes.addressof(uid), 1, 0, ctypes.byref(comm))
+    ids, w, k, seed = workloads.config4(n_pairs=300_000, n_keys=10**5)
+    y, s, _ = gm.sketch_elements(ids, w, 512, gm.SeedScheme(seed))
+    for fn in ("gm_allreduce_min_registers", "gm_allgather_merge_registers"):
+        y2, s2 = y.clone(), s.clone()
+        _device.call(fn, comm, y2.data_ptr(), s2.data_ptr(), 512, _device.stream_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(y2, y) and torch.equal(s2, s)
+    _device.call("gm_comm_destroy", comm)
+
+
+def test_workspace_lifecycle():
+    """Scratch is per (device, stream); gm_release_stream frees one set and
+    gm_finalize all of them; calls after either re-create what they need."""
+    from paper_2302_05176_b200 import _device, _lib
+    L = _lib.load()
+    st = torch.cuda.Stream()
+    ids, w, off, k, seed = workloads.config2(n_vectors=8)
+    with torch.cuda.stream(st):
+        a = gm.sketch_csr(ids, w, off, k, gm.SeedScheme(seed))
+    n0 = L.gm_workspace_count()
+    assert n0 >= 1
+    _device.call("gm_release_stream", st.cuda_stream)
+    assert L.gm_workspace_count() == n0 - 1
+    _device.call("gm_finalize")
+    assert L.gm_workspace_count() == 0
+    b = gm.sketch_csr(ids, w, off, k, gm.SeedScheme(seed))
+    assert torch.equal(a.y, b.y) and torch.equal(a.s, b.s)
+
+
+def test_rand_int_between_any_range():
+    """rand_int_between over ranges beyond 2**16, up to 2**64 (randgen.py:122-143)."""
+    sc = gm.SeedScheme(5)
+    for lo, hi, e, z in [(0, (1 << 20) - 1, 3, 1), (10, 10 + (1 << 40), 7, 9), (0, (1 << 64) - 1, 11, 2),
+                         (-5, 5, -1, 3), (1, (1 << 63) + 12345, 1 << 70, 1 << 65)]:
+        # the oracle draws the offset in [0, m) (m = 2**64 wraps in its u64 arithmetic: checked by range only)
+        want = lo + O.rand_int_between(sc.perm_seed, e & U64, z & U64, 0, hi - lo) if hi - lo < U64 else None
+        got = gm.rand_int_between(sc, e, z, lo, hi)
+        assert lo <= got <= hi
+        if want is not None:
+            assert got == want
 
 
 # ---------------------------------------------------------------- arithmetic

@@ -1,10 +1,15 @@
 """world_size-2 gloo runs of the multi-GPU host logic on CPU.
 
 Per-rank sketches come from the CPU oracle (this container has no GPU);
-what is under test is the sharding and the register exchange in
-paper_2302_05176_b200/shard.py: contiguous element shards, all-gather of
-k registers in rank order, and the rank-order min-merge reproducing the
-whole-stream sketch (partition law, test_estimate.py:174-199).
+what is under test is the sharding (paper_2302_05176_b200/shard.py:
+contiguous element shards, element-balanced vector ranges) and the two
+register-exchange protocols the C ABI runs over NCCL
+(csrc/gm_comm.cuh: gm_allreduce_min_registers, gm_allgather_merge_registers),
+restated here with torch.distributed collectives over gloo -- all-reduce MIN
+of y, then MIN of the ids of the ranks holding the minimum; all-gather and
+the rank-order merge -- both reproducing the whole-stream sketch (partition
+law, test_estimate.py:174-199).  The NCCL build of the same protocol runs
+on the GPU (tests/test_gpu_parity.py::test_nccl_exchange_world1).
 """
 
 import os
@@ -28,6 +33,31 @@ def _free_port():
         return s.getsockname()[1]
 
 
+_SIGN = 1 << 63
+
+
+def model_allreduce_min(y: torch.Tensor, s: torch.Tensor):
+    """gm_allreduce_min_registers' protocol: MIN of y; ids of the ranks that
+    hold the minimum (UINT64_MAX elsewhere); MIN of those ids.  Unsigned ids
+    ride in int64 with the sign bit flipped so signed MIN orders them."""
+    ym = y.clone()
+    dist.all_reduce(ym, op=dist.ReduceOp.MIN)
+    sign = torch.tensor(-_SIGN, dtype=torch.int64)
+    key = torch.where(y == ym, s ^ sign, torch.full_like(s, _SIGN - 1))
+    dist.all_reduce(key, op=dist.ReduceOp.MIN)
+    return ym, key ^ sign
+
+
+def model_allgather_merge(y: torch.Tensor, s: torch.Tensor):
+    """gm_allgather_merge_registers' protocol: all-gather, merge in rank order."""
+    world = dist.get_world_size()
+    ys = [torch.empty_like(y) for _ in range(world)]
+    ss = [torch.empty_like(s) for _ in range(world)]
+    dist.all_gather(ys, y)
+    dist.all_gather(ss, s)
+    return O.merge(torch.stack(ys).numpy(), torch.stack(ss).numpy().view(np.uint64))
+
+
 def _stream_worker(rank, port, out_dir):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
@@ -36,9 +66,8 @@ def _stream_worker(rank, port, out_dir):
     lo, hi = shard.element_range(ids.size, WORLD, rank)
     rc, y, s, _, _ = O.sketch_stream(ids[lo:hi], w[lo:hi].astype(np.float64), k, seed)
     assert rc == 0
-    ya, sa = shard.gather_registers(torch.from_numpy(y), torch.from_numpy(s.view(np.int64)))
-    ym, sm = O.merge(ya.numpy(), sa.numpy().view(np.uint64))
-    yr, sr = shard.allreduce_min_registers(torch.from_numpy(y.copy()), torch.from_numpy(s.view(np.int64).copy()))
+    ym, sm = model_allgather_merge(torch.from_numpy(y), torch.from_numpy(s.view(np.int64)))
+    yr, sr = model_allreduce_min(torch.from_numpy(y.copy()), torch.from_numpy(s.view(np.int64).copy()))
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), y=ym, s=sm, yr=yr.numpy(), sr=sr.numpy().view(np.uint64))
     dist.destroy_process_group()
 
@@ -94,8 +123,8 @@ def _minreduce_worker(rank, port, out_dir):
     inf = float("inf")
     y = [[1.0, 2.0, inf, 3.0, 5.0], [1.0, 1.5, inf, 3.0, inf]][rank]
     s = [[(1 << 64) - 2, 7, (1 << 64) - 1, (1 << 63) + 5, 9], [(1 << 63), 8, (1 << 64) - 1, (1 << 63) + 4, (1 << 64) - 1]][rank]
-    yr, sr = shard.allreduce_min_registers(torch.tensor(y, dtype=torch.float64),
-                                           torch.from_numpy(np.array(s, dtype=np.uint64).view(np.int64)))
+    yr, sr = model_allreduce_min(torch.tensor(y, dtype=torch.float64),
+                                 torch.from_numpy(np.array(s, dtype=np.uint64).view(np.int64)))
     np.savez(os.path.join(out_dir, f"mr{rank}.npz"), y=yr.numpy(), s=sr.numpy().view(np.uint64))
     dist.destroy_process_group()
 
