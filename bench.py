@@ -55,6 +55,10 @@ DIGESTS = os.path.join(ROOT, "tests", "golden", "full_digests.json")
 L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
 N_COPIES = 20  # resident input copies the timed batches rotate over (20 x 8 MB > L2)
 CONFIG1_SEEDS = 1000  # sketches of the config-1 vector per step (seeds 1..R)
+# gm_probe_arrival_rate variants: chains per thread (and the resident-CTA bound)
+PROBE_VARIANTS = {1: 1, 2: 2, 4: 4, 5: 1, 6: 2, 7: 1}
+PROBE_OCC = {1: "registers unbounded", 2: "registers unbounded", 4: "registers unbounded", 5: "8 CTAs/SM",
+             6: "6 CTAs/SM", 7: "6 CTAs/SM"}
 
 
 def parse():
@@ -222,9 +226,9 @@ def probe_peak(dev, k: int, stream):
     sink = torch.zeros(1, dtype=torch.float64, device=dev)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     best, best_c = 0.0, 0
-    for chains in (1, 2, 4):
+    for variant, chains in PROBE_VARIANTS.items():
         n_threads, iters = sms * 2048 // chains, 512
-        arg = iters | (chains << 24)
+        arg = iters | (variant << 24)
         for _ in range(2):
             _device.call("gm_probe_arrival_rate", n_threads, arg, k, sink.data_ptr(), stream.cuda_stream)
         torch.cuda.synchronize()
@@ -236,7 +240,7 @@ def probe_peak(dev, k: int, stream):
         torch.cuda.synchronize()
         rate = 5 * n_threads * chains * iters / (a0.elapsed_time(a1) / 1e3)
         if rate > best:
-            best, best_c = rate, chains
+            best, best_c = rate, f"{chains} chain(s)/thread, {PROBE_OCC[variant]}"
     return best, best_c
 
 
@@ -396,7 +400,7 @@ def csr_roofline(dev, stream, k, achieved_arrivals_per_s, alg_arrivals, executed
             "traffic": ev.get("dram_bytes_per_launch"),
             "peak_source": (f"gm_probe_arrival_rate in this run: the lane step's own arithmetic (hash, glibc-clone "
                             f"log, rounded product, branch-free divide, Barrett draw) at full occupancy, "
-                            f"{chains} chain(s)/thread, no pruning/tables/registers"),
+                            f"{chains}, no pruning/tables/registers"),
             "algorithmic_arrivals_per_launch": alg_arrivals, "executed_arrivals_per_launch": executed,
             "hbm": {"achieved_gbs": hbm_achieved, "peak_gbs": hbm, "peak_kind": hbm_kind, "frac": hbm_achieved / hbm}}
     for key in ("kernel_warp_inst_per_arrival", "probe_warp_inst_per_arrival", "probe_pipes", "kernel_pipes",

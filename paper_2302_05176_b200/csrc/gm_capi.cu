@@ -1085,19 +1085,26 @@ int gm_log_batch(const double* x, int64_t n, double* out, void* stream) {
 }
 
 int gm_probe_arrival_rate(int64_t n_threads, int32_t iters, int32_t k, double* sink, void* stream) {
-  // n_threads threads, each walking `chains` element queues (chains = 1, 2
-  // or 4 from the high bits of iters: iters | chains << 24) for `iters` arrivals
+  // n_threads threads, each walking C element queues for `iters` arrivals;
+  // iters | variant << 24 selects (C, resident CTAs per SM):
+  // 0, 2: (2, any)  1: (1, any)  4: (4, any)  5: (1, 8)  6: (2, 6)  7: (1, 6)
   g_msg[0] = 0;
   (void)cudaGetLastError();
-  const int chains = (iters >> 24) ? (iters >> 24) : 2;
+  const int variant = iters >> 24;
   iters &= 0xFFFFFF;
-  if (k < 128 || k > 65536 || iters < 1 || n_threads < NT || (chains != 1 && chains != 2 && chains != 4))
+  if (k < 128 || k > 65536 || iters < 1 || n_threads < NT || variant == 3 || variant > 7)
     return fail(GM_ERR_INVALID_PARAMETER, "bad probe arguments");
   const unsigned grid = (unsigned)(n_threads / NT);
   cudaStream_t st = (cudaStream_t)stream;
-  if (chains == 1) arrival_probe_kernel<1><<<grid, NT, 0, st>>>(iters, (u32)k, 0x1234ull, 0x5678ull, sink);
-  else if (chains == 2) arrival_probe_kernel<2><<<grid, NT, 0, st>>>(iters, (u32)k, 0x1234ull, 0x5678ull, sink);
-  else arrival_probe_kernel<4><<<grid, NT, 0, st>>>(iters, (u32)k, 0x1234ull, 0x5678ull, sink);
+  const u32 kk = (u32)k;
+  switch (variant) {
+    case 1: arrival_probe_kernel<1><<<grid, NT, 0, st>>>(iters, kk, 0x1234ull, 0x5678ull, sink); break;
+    case 4: arrival_probe_kernel<4><<<grid, NT, 0, st>>>(iters, kk, 0x1234ull, 0x5678ull, sink); break;
+    case 5: arrival_probe_kernel<1, 8><<<grid, NT, 0, st>>>(iters, kk, 0x1234ull, 0x5678ull, sink); break;
+    case 6: arrival_probe_kernel<2, 6><<<grid, NT, 0, st>>>(iters, kk, 0x1234ull, 0x5678ull, sink); break;
+    case 7: arrival_probe_kernel<1, 6><<<grid, NT, 0, st>>>(iters, kk, 0x1234ull, 0x5678ull, sink); break;
+    default: arrival_probe_kernel<2><<<grid, NT, 0, st>>>(iters, kk, 0x1234ull, 0x5678ull, sink); break;
+  }
   CK(cudaGetLastError());
   return GM_OK;
 }

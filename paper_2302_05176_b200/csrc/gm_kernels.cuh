@@ -912,8 +912,8 @@ __global__ void log_batch_kernel(const double* x, int64_t n, double* out) {
 // table -- with no pruning, no Fisher-Yates table, no register update, no
 // queue bookkeeping and no memory traffic.  C chains per thread give the
 // scheduler independent work (ILP) on top of full occupancy.
-template <int C>
-__global__ void __launch_bounds__(NT) arrival_probe_kernel(int iters, u32 k, u64 useed, u64 pseed, double* sink) {
+template <int C, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) arrival_probe_kernel(int iters, u32 k, u64 useed, u64 pseed, double* sink) {
   __shared__ __align__(16) double ltab[256];
   __shared__ u64 mtab64[128];
   for (u32 i = threadIdx.x; i < 256; i += NT) ltab[i] = gm_glog_tab[i >> 1][i & 1];

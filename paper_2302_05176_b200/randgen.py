@@ -125,10 +125,10 @@ def rand_int_between(scheme: SeedScheme, element: int, step: int, lo: int, hi: i
         # the reference's rejection bound 2**64 - 2**64 % m is 0 here: it never returns
         raise ValueError("ranges wider than 2**64 have no accepted draw")
     dev = _device.require_cuda()
-    t = lambda v: _u64_tensor([v & ((1 << 64) - 1)], dev)  # noqa: E731
+    # the four key arrays stay referenced until the call returns (it synchronises)
+    keys = [_u64_tensor([v & MASK64], dev) for v in (scheme.perm_seed, element, step, m - 1)]
     out = torch.empty(1, dtype=torch.int64, device=dev)
-    _device.call("gm_rand_int_between_batch", t(scheme.perm_seed).data_ptr(), t(element).data_ptr(),
-                 t(step).data_ptr(), t(m - 1).data_ptr(), 1, out.data_ptr(), _device.stream_ptr())
+    _device.call("gm_rand_int_between_batch", *(a.data_ptr() for a in keys), 1, out.data_ptr(), _device.stream_ptr())
     return lo + (int(out.cpu().item()) & ((1 << 64) - 1))
 
 

@@ -728,6 +728,23 @@ def test_rand_int_between_any_range():
             assert got == want
 
 
+def test_service_exchanges_byte_identical():
+    """The reference service's sketch and estimator routes (service/app.py:74-118)
+    served by the CUDA engine (paper_2302_05176_b200.service): every recorded
+    exchange of the reference's own app (tests/golden/make_service_golden.py)
+    -- vector sketches (fast, naive, salted, a 5,000-entry vector that runs
+    grid-wide), stream sketches, merges, estimators and the 400 errors --
+    gives the same status and the same response bytes."""
+    from fastapi.testclient import TestClient
+
+    from paper_2302_05176_b200.service import create_app
+    client = TestClient(create_app())
+    for ex in load_json("service_exchanges.json"):
+        r = client.get(ex["path"]) if ex["method"] == "GET" else client.post(ex["path"], json=ex["request"])
+        assert r.status_code == ex["status"], (ex["path"], r.text[:200])
+        assert r.text == ex["body"], (ex["path"], r.text[:200], ex["body"][:200])
+
+
 # ---------------------------------------------------------------- arithmetic
 def test_branch_free_divide_equals_ieee_divide():
     """ddiv_fast (the lane walkers' divide) == __ddiv_rn on its weight range."""
