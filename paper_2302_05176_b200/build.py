@@ -32,17 +32,20 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Build the library (to `out` with extra -D `defines` for tuning and
+    instrumented builds; the product build takes neither)."""
+    if out is None and not defines and not force and up_to_date():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT, *SOURCES, "-lcudart", "-ldl"]
+    out = out or OUT
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", out, *SOURCES, "-lcudart", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libgmsketch_b200.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

@@ -167,11 +167,19 @@ int num_sms() {
   return sms > 0 ? sms : 148;
 }
 
-using CsrDefault = CsrCfg<256, 16, 2, 2, 75, 4>;
+// (GM_DEEP_PCT / GM_DRAIN: compile-time overrides for tuning builds only;
+// the product build uses the defaults)
+#ifndef GM_DEEP_PCT
+#define GM_DEEP_PCT 75
+#endif
+#ifndef GM_DRAIN
+#define GM_DRAIN 4
+#endif
+using CsrDefault = CsrCfg<256, 16, 2, 2, GM_DEEP_PCT, GM_DRAIN>;
 // k <= 512: four vector slots fit in the shared memory two slots of k = 1024
 // take, so a CTA keeps four (small) vectors in flight -- fewer lanes idle
 // while a slot drains (config 3: 19.4 -> 16.4 ms per batch)
-using CsrSmallK = CsrCfg<256, 16, 4, 2, 75, 4>;
+using CsrSmallK = CsrCfg<256, 16, 4, 2, GM_DEEP_PCT, GM_DRAIN>;
 
 template <class C, class IdT, class WT>
 int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k,
