@@ -251,6 +251,18 @@ int gm_rand_int_between_batch(const uint64_t *perm_seeds, const uint64_t *elemen
                               const uint64_t *steps, const uint64_t *m_minus_1,
                               int64_t n, uint64_t *out, void *stream);
 
+/* ElementQueueState / next_order_statistic (randgen.py:210-271) on the device:
+ * n queues of k customers each advance `steps` emissions.  Queue i is element
+ * elements[i] with weight weights[i], z0[i] order statistics already emitted,
+ * the last at time b0[i]; perm + i*k is its Fisher-Yates array (values 1..k,
+ * swapped in place).  Emission q of queue i: t_out[i*steps+q] (arrival time)
+ * and s_out[i*steps+q] (server, 1..k); b_out[i] = the last time.  The caller
+ * keeps z0[i] + steps <= k.  (device) arrays; asynchronous. */
+int gm_queue_advance_batch(const uint64_t *elements, const double *weights, const int32_t *z0,
+                           const double *b0, int64_t n, int32_t k, int32_t steps,
+                           uint64_t global_seed, uint64_t stream_salt, uint32_t *perm,
+                           double *t_out, uint32_t *s_out, double *b_out, void *stream);
+
 /* Arithmetic self-checks (device).
  * gm_arith_check: over n keyed random inputs, counts[0] = #(branch-free
  * divide != IEEE __ddiv_rn) on the fast weight range, counts[1] = #(device
@@ -276,24 +288,14 @@ int gm_check_pairs(const void *ids, int id_bits, const void *w, int w_bits,
                    void *uniq_ids, void *uniq_w, int64_t *n_uniq,
                    void *stream);
 
-/* One element queue advanced on the host (ElementQueueState /
- * next_order_statistic, randgen.py:210-271, over _run_queue :158-207):
- * emissions z0+1 .. z0+steps of `element` (weight w, k servers) from running
- * time b0; perm (host, k entries: the Fisher-Yates array, values 1..k) is
- * updated in place; t_out[i], s_out[i] = emitted time and server.  glibc log,
- * the reference's operation order.  Host memory only; no CUDA. */
-int gm_queue_advance(uint64_t global_seed, uint64_t stream_salt,
-                     uint64_t element, double w, int32_t k, int32_t z0,
-                     int32_t steps, double b0, uint32_t *perm, double *t_out,
-                     uint32_t *s_out);
-
 /* Exact-y finalize (host memory only; no CUDA): y_io[v*k + j] := the
  * arrival time the reference computes for register j of CSR vector v,
  * given its winning element s[v*k + j] (from gm_sketch_csr* /
  * gm_sketch_elements), by walking that element's queue with glibc log and
  * IEEE double arithmetic in the reference's operation order
- * (randgen.py:158-207).  The device's y can differ from the reference's by
- * an ulp (its log is CUDA's); after this call y is bit-identical.  Every
+ * (randgen.py:158-207).  A host cross-check: the device's y already carries
+ * these bits (its log is glibc's, gm_glibc_log.cuh), and no entry point calls
+ * it.  Every
  * s must name an element of its vector (else GM_ERR_MISMATCHED).  For a
  * stream, pass n_vec = 1 and offsets {0, n}.  n_threads <= 0: all host
  * threads.  Replaces the float equality of GumbelMaxSketch

@@ -41,6 +41,7 @@ from .randgen import (
     DEFAULT_STREAM_SALT,
     ElementQueueState,
     LazyPermutation,
+    advance_queues,
     SeedScheme,
     derive_seed,
     mix64,

@@ -66,7 +66,7 @@ SIGNATURES = {
     "gm_arith_check": (_int, [_i64, _u64, _vp, _vp]),
     "gm_log_batch": (_int, [_vp, _i64, _vp, _vp]),
     "gm_check_pairs": (_int, [_vp, _int, _vp, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "gm_queue_advance": (_int, [_u64, _u64, _u64, _dbl, _i32, _i32, _i32, _dbl, _vp, _vp, _vp]),
+    "gm_queue_advance_batch": (_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _u64, _u64, _vp, _vp, _vp, _vp, _vp]),
     "gm_exact_y": (_int, [_vp, _int, _vp, _int, _vp, _i64, _i32, _u64, _u64, _vp, _vp, _i32]),
     "gm_probe_arrival_rate": (_int, [_i64, _i32, _i32, _vp, _vp]),
     "gm_count_arrivals_csr": (_int, [_vp, _int, _vp, _int, _vp, _i64, _i32, _u64, _vp, _vp, _vp]),

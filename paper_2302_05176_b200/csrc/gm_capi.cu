@@ -1071,6 +1071,20 @@ int gm_rand_int_between_batch(const uint64_t* perm_seeds, const uint64_t* elemen
   return GM_OK;
 }
 
+int gm_queue_advance_batch(const uint64_t* elements, const double* weights, const int32_t* z0, const double* b0,
+                           int64_t n, int32_t k, int32_t steps, uint64_t global_seed, uint64_t stream_salt,
+                           uint32_t* perm, double* t_out, uint32_t* s_out, double* b_out, void* stream) {
+  g_msg[0] = 0;
+  (void)cudaGetLastError();
+  if (k < 1 || k > 65536 || steps < 0 || n < 0)
+    return fail(GM_ERR_INVALID_PARAMETER, "gm_queue_advance_batch: k in [1, 65536], steps >= 0, n >= 0");
+  if (n == 0 || steps == 0) return GM_OK;
+  queue_advance_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      elements, weights, z0, b0, n, (u32)k, steps, global_seed, global_seed ^ stream_salt, perm, t_out, s_out, b_out);
+  CK(cudaGetLastError());
+  return GM_OK;
+}
+
 int gm_arith_check(int64_t n, uint64_t seed, unsigned long long* counts, void* stream) {
   g_msg[0] = 0;
   (void)cudaGetLastError();

@@ -177,33 +177,6 @@ int exact_all(const IdT* ids, const WT* w, const int64_t* offsets, int64_t n_vec
 // ElementQueueState randgen.py:210-271): perm holds the k entries of the
 // permutation (1-based values) and is updated in place; t_out/s_out receive
 // the emitted (time, server) pairs.  Host memory only.
-extern "C" int gm_queue_advance(uint64_t global_seed, uint64_t stream_salt, uint64_t element, double w, int32_t k,
-                                int32_t z0, int32_t steps, double b0, uint32_t* perm, double* t_out,
-                                uint32_t* s_out) {
-  if (k < 1 || z0 < 0 || steps < 0 || z0 + steps > k || !(w > 0.0) || !std::isfinite(w))
-    return GM_ERR_INVALID_PARAMETER;
-  const u64 ubase = global_seed + element * kElem, pbase = (global_seed ^ stream_salt) + element * kElem;
-  double b = b0;
-  for (int32_t i = 0; i < steps; ++i) {
-    const u32 z = (u32)(z0 + i + 1);
-    const u64 x = splitmix(ubase + (u64)z * kStep);
-    const double u = (double)(x >> 11) * 0x1p-53 + 0x1p-54;
-    const u32 mz = (u32)k - z + 1;
-    b = b + (-std::log(u)) / (w * (double)mz);
-    const u64 m = mz;
-    const u64 rem = (UINT64_MAX % m + 1) % m;
-    u64 g = splitmix(pbase + (u64)z * kStep);
-    for (u64 a = 1; rem != 0 && g >= (u64)0 - rem; ++a) g = splitmix(pbase + (u64)z * kStep + a * kRetry);
-    const u32 jpos = (u32)(z - 1 + g % m);
-    const u32 vz = perm[z - 1];
-    perm[z - 1] = perm[jpos];
-    perm[jpos] = vz;
-    t_out[i] = b;
-    s_out[i] = perm[z - 1];
-  }
-  return GM_OK;
-}
-
 extern "C" int gm_exact_y(const void* ids, int id_bits, const void* w, int w_bits, const int64_t* offsets,
                           int64_t n_vec, int32_t k, uint64_t global_seed, uint64_t stream_salt,
                           const uint64_t* s, double* y_io, int32_t n_threads) {

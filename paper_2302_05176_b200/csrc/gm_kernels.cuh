@@ -868,6 +868,34 @@ __global__ void randint_general_kernel(const u64* pseeds, const u64* elems, cons
   out[i] = x % m;
 }
 
+// ElementQueueState / next_order_statistic (randgen.py:210-271) on the device:
+// queue i emits `steps` order statistics from its cursor (z0[i] emitted, last
+// time b0[i]), swapping its dense Fisher-Yates array perm[i*k .. i*k+k)
+// (values 1..k) in place: the reference's _run_queue arithmetic
+// (randgen.py:181-203) with glibc's log.  One thread per queue.
+__global__ void queue_advance_kernel(const u64* __restrict__ elems, const double* __restrict__ w,
+                                     const int32_t* __restrict__ z0, const double* __restrict__ b0, int64_t n, u32 k,
+                                     int32_t steps, u64 useed, u64 pseed, u32* __restrict__ perm,
+                                     double* __restrict__ t_out, u32* __restrict__ s_out, double* __restrict__ b_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u64 ubase = useed + elems[i] * K_ELEM, pbase = pseed + elems[i] * K_ELEM;
+  u32* P = perm + i * (int64_t)k;
+  double b = b0[i];
+  for (int32_t q = 0; q < steps; ++q) {
+    const u32 z = (u32)z0[i] + (u32)q + 1u;
+    const double L = -log_pos(u_open(mix64(ubase + (u64)z * K_STEP)));
+    b = __dadd_rn(b, __ddiv_rn(L, __dmul_rn(w[i], (double)(k - z + 1))));
+    const u32 jpos = perm_draw(pbase, z, k) - 1;
+    const u32 vz = P[z - 1];
+    P[z - 1] = P[jpos];
+    P[jpos] = vz;
+    t_out[i * steps + q] = b;
+    s_out[i * steps + q] = P[z - 1];
+  }
+  b_out[i] = b;
+}
+
 // ---- arithmetic self-check: ddiv_fast == __ddiv_rn on the fast range, and
 // log_pos within 1 ulp of CUDA's log, over keyed random inputs ----
 __global__ void arith_check_kernel(int64_t n, u64 seed, unsigned long long* counts) {

@@ -135,10 +135,9 @@ def rand_int_between(scheme: SeedScheme, element: int, step: int, lo: int, hi: i
 class ElementQueueState:
     """Generation cursor for one element's queue of k customers
     (randgen.py:210-242): emitted count z, last emitted value b, and the
-    Fisher-Yates array perm (values 1..k).  Advanced on the host by
-    gm_queue_advance with the reference's arithmetic (this is the
-    reference's one-emission-at-a-time API surface; the sketch kernels never
-    use it)."""
+    Fisher-Yates array perm (values 1..k, a uint32 array).  Advanced on the
+    device (gm_queue_advance_batch: the reference's _run_queue arithmetic,
+    glibc log included)."""
 
     def __init__(self, element_id: int, weight: float, k: int, z: int = 0, b: float = 0.0, perm=None):
         from .errors import InvalidWeightError
@@ -161,20 +160,45 @@ class ElementQueueState:
         return self.z >= self.k
 
 
-def next_order_statistic(state: ElementQueueState, scheme: SeedScheme) -> tuple[float, int]:
-    """Advance a queue by one emission; (arrival time, server) (randgen.py:245-271)."""
-    from . import _lib
+def advance_queues(states, scheme: SeedScheme, steps: int = 1):
+    """Advance every ElementQueueState of `states` (same k) by `steps`
+    emissions in one device launch (gm_queue_advance_batch); returns
+    (times [n, steps] float64, servers [n, steps] int64) and updates the
+    states (z, b, perm) in place."""
     from .errors import QueueExhaustedError
 
-    if state.z >= state.k:
-        raise QueueExhaustedError(f"element {state.element_id}: all {state.k} order statistics emitted")
-    t = np.zeros(1, np.float64)
-    srv = np.zeros(1, np.uint32)
-    rc = _lib.load().gm_queue_advance(scheme.global_seed, scheme.stream_salt, state.element_id & MASK64,
-                                      state.weight, state.k, state.z, 1, state.b, state.perm.ctypes.data,
-                                      t.ctypes.data, srv.ctypes.data)
-    if rc:
-        raise ValueError(f"gm_queue_advance failed ({rc})")
-    state.z += 1
-    state.b = float(t[0])
-    return state.b, int(srv[0])
+    states = list(states)
+    if not states:
+        return np.zeros((0, steps)), np.zeros((0, steps), np.int64)
+    k = states[0].k
+    if any(st.k != k for st in states):
+        raise ValueError("advance_queues: every queue must have the same k")
+    for st in states:
+        if st.z + steps > k:
+            raise QueueExhaustedError(f"element {st.element_id}: all {st.k} order statistics emitted")
+    dev = _device.require_cuda()
+    n = len(states)
+    el = _u64_tensor([st.element_id for st in states], dev)
+    w = torch.tensor([st.weight for st in states], dtype=torch.float64, device=dev)
+    z0 = torch.tensor([st.z for st in states], dtype=torch.int32, device=dev)
+    b0 = torch.tensor([st.b for st in states], dtype=torch.float64, device=dev)
+    perm = torch.from_numpy(np.stack([st.perm for st in states]).view(np.int32)).to(dev)
+    t = torch.empty((n, steps), dtype=torch.float64, device=dev)
+    s = torch.empty((n, steps), dtype=torch.int32, device=dev)
+    bo = torch.empty(n, dtype=torch.float64, device=dev)
+    _device.call("gm_queue_advance_batch", el.data_ptr(), w.data_ptr(), z0.data_ptr(), b0.data_ptr(), n, k, steps,
+                 scheme.global_seed, scheme.stream_salt, perm.data_ptr(), t.data_ptr(), s.data_ptr(), bo.data_ptr(),
+                 _device.stream_ptr())
+    perm_h = perm.cpu().numpy().view(np.uint32)
+    b_h = bo.cpu().numpy()
+    for i, st in enumerate(states):
+        st.perm = np.ascontiguousarray(perm_h[i])
+        st.z += steps
+        st.b = float(b_h[i])
+    return t.cpu().numpy(), s.cpu().numpy().astype(np.int64)
+
+
+def next_order_statistic(state: ElementQueueState, scheme: SeedScheme) -> tuple[float, int]:
+    """Advance a queue by one emission; (arrival time, server) (randgen.py:245-271)."""
+    t, s = advance_queues([state], scheme, 1)
+    return float(t[0, 0]), int(s[0, 0])

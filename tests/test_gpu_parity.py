@@ -745,6 +745,32 @@ def test_service_exchanges_byte_identical():
         assert r.text == ex["body"], (ex["path"], r.text[:200], ex["body"][:200])
 
 
+def test_element_queue_state_on_device_matches_reference_queues():
+    """ElementQueueState / next_order_statistic on the device (gm_queue_advance_batch)
+    against the reference's full queues (tests/golden/rng_kats.json): bit-identical
+    times and servers; QueueExhaustedError after k.  And advance_queues over many
+    queues at once against the oracle's _run_queue."""
+    for q in load_json("rng_kats.json")["queues"]:
+        sc = gm.SeedScheme(q["seed"])
+        st = gm.ElementQueueState(q["element"], float.fromhex(q["weight"]) if isinstance(q["weight"], str)
+                                  else q["weight"], q["k"])
+        got = [gm.next_order_statistic(st, sc) for _ in range(q["k"])]
+        assert [t for t, _ in got] == hexs(q["times"]).tolist()
+        assert [s for _, s in got] == list(q["servers"])
+        assert st.exhausted and sorted(st.perm.tolist()) == list(range(1, q["k"] + 1))
+        with pytest.raises(gm.QueueExhaustedError):
+            gm.next_order_statistic(st, sc)
+    sc = gm.SeedScheme(17)
+    k = 300
+    states = [gm.ElementQueueState(e, 0.1 + e / 7.0, k) for e in range(1, 65)]
+    t1, s1 = gm.advance_queues(states, sc, 100)
+    t2, s2 = gm.advance_queues(states, sc, 200)
+    t, s = np.concatenate([t1, t2], axis=1), np.concatenate([s1, s2], axis=1)
+    for i, e in enumerate(range(1, 65)):
+        to, so = O.run_queue_full(17, sc.stream_salt, e, 0.1 + e / 7.0, k)
+        assert t[i].tobytes() == to.tobytes() and s[i].tolist() == so.tolist()
+
+
 # ---------------------------------------------------------------- arithmetic
 def test_branch_free_divide_equals_ieee_divide():
     """ddiv_fast (the lane walkers' divide) == __ddiv_rn on its weight range."""
