@@ -25,6 +25,10 @@
 
 using namespace gmk;
 
+// registers per sketch: up to 2^24 (256 MB of (y, s) registers; queues of more
+// than 65536 customers run on the grid-wide kernels with 64-bit Fisher-Yates words)
+constexpr int32_t GM_K_MAX = 1 << 24;
+
 namespace {
 
 thread_local char g_msg[512] = "";
@@ -236,11 +240,11 @@ int check_common(int id_bits, int w_bits, int32_t k) {
   if (id_bits != 32 && id_bits != 64) return fail(GM_ERR_INVALID_PARAMETER, "id_bits must be 32 or 64, got %d", id_bits);
   if (w_bits != 32 && w_bits != 64) return fail(GM_ERR_INVALID_PARAMETER, "w_bits must be 32 or 64, got %d", w_bits);
   if (k < 1) return fail(GM_ERR_INVALID_PARAMETER, "InvalidParameterError: k must be >= 1, got %d", k);
-  if (k > 65536) return fail(GM_ERR_INVALID_PARAMETER, "k=%d exceeds the supported maximum 65536", k);
+  if (k > GM_K_MAX) return fail(GM_ERR_INVALID_PARAMETER, "k=%d exceeds the supported maximum %d", k, GM_K_MAX);
   return GM_OK;
 }
 
-template <class IdT, class WT>
+template <class IdT, class WT, class W>
 int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u64 pseed,
                  uint32_t flags, double* y_io, u64* s_io, int64_t* emitted_out, Workspace* ws,
                  cudaStream_t st, int* unset_async = nullptr) {
@@ -284,11 +288,15 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
     const int64_t heavy_need = std::min<int64_t>(n, (int64_t)1 << 22);
     rc = grow(&ws->heavy, &ws->heavy_cap, (size_t)heavy_need, st);
     if (rc) return rc;
-    const int64_t heavy_blocks = (int64_t)num_sms() * 4;
-    rc = grow(&ws->dense, &ws->dense_cap, (size_t)heavy_blocks * NWARP * k, st, true);
+    // per-warp dense Fisher-Yates arrays of the heavy walk (k words each); for
+    // large k the grid shrinks so the scratch stays <= 1 GB
+    const int64_t heavy_blocks = std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)num_sms() * 4, ((int64_t)1 << 30) / ((int64_t)NWARP * k * (int64_t)sizeof(W))));
+    rc = grow(&ws->dense, &ws->dense_cap, (size_t)heavy_blocks * NWARP * k * (sizeof(W) / 4), st, true);
     if (rc) return rc;
+    W* dense = reinterpret_cast<W*>(ws->dense);
     int light_per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&light_per_sm, elem_light_kernel<IdT, WT>, NT, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&light_per_sm, elem_light_kernel<IdT, WT, W>, NT, 0));
     int64_t lgrid = (int64_t)light_per_sm * num_sms();
     lgrid = std::min<int64_t>(lgrid, (n + NT - 1) / NT);
     // filter pass (HBM-streaming first-arrival test against the list bound
@@ -301,17 +309,17 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
     if ((rc = grow(&ws->surv, &ws->surv_cap, (size_t)surv_cap, st))) return rc;
     const int64_t fgrid = std::min<int64_t>((n / 4 + 2 * NT - 1) / (2 * NT) + 1, (int64_t)num_sms() * 8);
     int surv_per_sm = 0;  // the list walk is latency-bound: as many resident CTAs as fit
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&surv_per_sm, elem_survivor_kernel, NT, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&surv_per_sm, elem_survivor_kernel<W>, NT, 0));
     surv_per_sm = std::max(surv_per_sm, 1);
     if (unset_async) {  // one pass at the list bound, nothing read back
       elem_filter_kernel<IdT, WT><<<(unsigned)fgrid, NT, 0, st>>>(
           (const IdT*)ids, (const WT*)w, n, k, useed, ws->dbl + 3, ws->surv, surv_cap, ws->ull + 2, nullptr, ws->err);
-      elem_survivor_kernel<<<(unsigned)(num_sms() * surv_per_sm), NT, 0, st>>>(
+      elem_survivor_kernel<W><<<(unsigned)(num_sms() * surv_per_sm), NT, 0, st>>>(
           ws->surv, ws->ull + 2, surv_cap, k, useed, pseed, ws->dbl, ws->regs, ws->counters + 1, ws->heavy,
           (int64_t)ws->heavy_cap, ws->ull, nullptr);
-      elem_heavy_kernel<IdT, WT><<<(unsigned)heavy_blocks, NT, 0, st>>>(
+      elem_heavy_kernel<IdT, WT, W><<<(unsigned)heavy_blocks, NT, 0, st>>>(
           (const IdT*)ids, (const WT*)w, ws->surv, k, useed, pseed, ws->dbl, ws->regs, ws->counters + 1, ws->heavy,
-          ws->ull, (int64_t)ws->heavy_cap, ws->dense, nullptr, (unsigned*)(ws->counters + 2), y_io, s_io);
+          ws->ull, (int64_t)ws->heavy_cap, dense, nullptr, (unsigned*)(ws->counters + 2), y_io, s_io);
       CK(cudaGetLastError());
       CK(cudaMemcpyAsync(unset_async, ws->counters + 1, sizeof(int), cudaMemcpyDeviceToDevice, st));
       return GM_OK;
@@ -352,20 +360,20 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
                 ws->ull + 2, emitted_out ? ws->ull + 1 : nullptr, ws->err);
             CK(cudaGetLastError());
           }
-          elem_survivor_kernel<<<(unsigned)(num_sms() * surv_per_sm), NT, 0, st>>>(
+          elem_survivor_kernel<W><<<(unsigned)(num_sms() * surv_per_sm), NT, 0, st>>>(
               ws->surv, ws->ull + 2, surv_cap, k, useed, pseed, ws->dbl,
               ws->regs, ws->counters + 1, ws->heavy, (int64_t)ws->heavy_cap, ws->ull,
               emitted_out ? ws->ull + 1 : nullptr);
         } else {
-          elem_light_kernel<IdT, WT><<<(unsigned)lgrid, NT, 0, st>>>(
+          elem_light_kernel<IdT, WT, W><<<(unsigned)lgrid, NT, 0, st>>>(
               (const IdT*)ids, (const WT*)w, n, k, useed, pseed, ws->dbl, ws->regs, ws->counters + 1,
               ws->heavy, (int64_t)ws->heavy_cap, ws->ull, emitted_out ? ws->ull + 1 : nullptr, ws->err);
         }
         CK(cudaGetLastError());
-        elem_heavy_kernel<IdT, WT><<<(unsigned)heavy_blocks, NT, 0, st>>>(
+        elem_heavy_kernel<IdT, WT, W><<<(unsigned)heavy_blocks, NT, 0, st>>>(
             (const IdT*)ids, (const WT*)w, use_filter ? ws->surv : nullptr, k, useed, pseed, ws->dbl, ws->regs,
             ws->counters + 1,
-            ws->heavy, ws->ull, (int64_t)ws->heavy_cap, ws->dense,
+            ws->heavy, ws->ull, (int64_t)ws->heavy_cap, dense,
             emitted_out ? ws->ull + 1 : nullptr, (unsigned*)(ws->counters + 2), y_io, s_io);
         // (its last CTA stores the registers: with every attempt, a no-op
         // rewrite when another follows, so a single-attempt call synchronises once)
@@ -424,6 +432,26 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
   CK(cudaStreamSynchronize(st));
   if (emitted_out) *emitted_out = 0;
   return GM_OK;
+}
+
+// K2 for every id/weight width; queues of more than 65536 customers use
+// 64-bit Fisher-Yates words (32-bit positions and values) and exact 64-bit draws
+int dispatch_elements(const void* ids, int id_bits, const void* w, int w_bits, int64_t n, u32 k, u64 useed,
+                      u64 pseed, uint32_t flags, double* y_io, u64* s_io, int64_t* emitted_out, Workspace* ws,
+                      cudaStream_t st, int* unset_async) {
+#define GM_ELEM_RUN(I, F, W) \
+  return run_elements<I, F, W>(ids, w, n, k, useed, pseed, flags, y_io, s_io, emitted_out, ws, st, unset_async)
+  if (k <= 65536u) {
+    if (id_bits == 32 && w_bits == 32) GM_ELEM_RUN(u32, float, u32);
+    if (id_bits == 32) GM_ELEM_RUN(u32, double, u32);
+    if (w_bits == 32) GM_ELEM_RUN(u64, float, u32);
+    GM_ELEM_RUN(u64, double, u32);
+  }
+  if (id_bits == 32 && w_bits == 32) GM_ELEM_RUN(u32, float, u64);
+  if (id_bits == 32) GM_ELEM_RUN(u32, double, u64);
+  if (w_bits == 32) GM_ELEM_RUN(u64, float, u64);
+  GM_ELEM_RUN(u64, double, u64);
+#undef GM_ELEM_RUN
 }
 
 }  // namespace
@@ -924,14 +952,8 @@ int gm_sketch_elements(const void* ids, int id_bits, const void* w, int w_bits, 
   if (rc) return rc;
   const u64 useed = global_seed, pseed = global_seed ^ stream_salt;
   const u32 kk = (u32)k;
-  if (id_bits == 32 && w_bits == 32)
-    rc = run_elements<u32, float>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, emitted_out, ws, st);
-  else if (id_bits == 32)
-    rc = run_elements<u32, double>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, emitted_out, ws, st);
-  else if (w_bits == 32)
-    rc = run_elements<u64, float>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, emitted_out, ws, st);
-  else
-    rc = run_elements<u64, double>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, emitted_out, ws, st);
+  rc = dispatch_elements(ids, id_bits, w, w_bits, n, kk, useed, pseed, flags, y_io, s_io, emitted_out, ws, st,
+                         nullptr);
   if (rc) return rc;
   const int unset = (int)(ws->host[0] & 0xFFFFFFFFull);
   if (unset > 0)
@@ -956,13 +978,8 @@ int gm_sketch_elements_async(const void* ids, int id_bits, const void* w, int w_
   if (rc) return rc;
   const u64 useed = global_seed, pseed = global_seed ^ stream_salt;
   const u32 kk = (u32)k;
-  if (id_bits == 32 && w_bits == 32)
-    return run_elements<u32, float>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, nullptr, ws, st, unset_out);
-  if (id_bits == 32)
-    return run_elements<u32, double>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, nullptr, ws, st, unset_out);
-  if (w_bits == 32)
-    return run_elements<u64, float>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, nullptr, ws, st, unset_out);
-  return run_elements<u64, double>(ids, w, n, kk, useed, pseed, flags, y_io, s_io, nullptr, ws, st, unset_out);
+  return dispatch_elements(ids, id_bits, w, w_bits, n, kk, useed, pseed, flags, y_io, s_io, nullptr, ws, st,
+                           unset_out);
 }
 
 int gm_sketch_elements_host(const void* ids, int id_bits, const void* w, int w_bits, int64_t n,
@@ -1076,8 +1093,8 @@ int gm_queue_advance_batch(const uint64_t* elements, const double* weights, cons
                            uint32_t* perm, double* t_out, uint32_t* s_out, double* b_out, void* stream) {
   g_msg[0] = 0;
   (void)cudaGetLastError();
-  if (k < 1 || k > 65536 || steps < 0 || n < 0)
-    return fail(GM_ERR_INVALID_PARAMETER, "gm_queue_advance_batch: k in [1, 65536], steps >= 0, n >= 0");
+  if (k < 1 || k > GM_K_MAX || steps < 0 || n < 0)
+    return fail(GM_ERR_INVALID_PARAMETER, "gm_queue_advance_batch: k in [1, %d], steps >= 0, n >= 0", GM_K_MAX);
   if (n == 0 || steps == 0) return GM_OK;
   queue_advance_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
       elements, weights, z0, b0, n, (u32)k, steps, global_seed, global_seed ^ stream_salt, perm, t_out, s_out, b_out);

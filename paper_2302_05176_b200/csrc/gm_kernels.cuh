@@ -63,18 +63,18 @@ __device__ __forceinline__ double pass_tau(double W, u32 k, int attempt) {
 // ---- K2: one huge element set, registers in global memory ---------------
 // light pass: grid-stride, one thread per element; heavy/overflowing
 // elements are appended to heavy_list and walked by elem_heavy_kernel.
-template <class IdT, class WT>
+template <class IdT, class WT, class W = u32>
 __global__ void __launch_bounds__(NT)
     elem_light_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, int64_t n, u32 k,
                       u64 useed, u64 pseed, const double* __restrict__ tau_p, Reg* regs,
                       int* unset_ctr, u64* __restrict__ heavy_list, int64_t heavy_cap,
                       unsigned long long* heavy_count, unsigned long long* emitted_total,
                       unsigned long long* __restrict__ err) {
-  __shared__ u32 maps[16 * NT];
+  __shared__ W maps[16 * NT];
   const double tau = *tau_p;
   const double light_w = 8.0 / ((double)k * tau);
   u32 emitted = 0;
-  u32* mymap = maps + threadIdx.x;
+  W* mymap = maps + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * NT;
   // four coalesced loads in flight per thread, then the cheap first-arrival
   // filter; the rare survivors walk their queues
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(NT)
       }
       bool ok = false;
       if (w < light_w)
-        ok = walk_light<false>(id, w, tau, k, useed, pseed, mymap, NT, 16, regs, unset_ctr, emitted);
+        ok = walk_light<false, W>(id, w, tau, k, useed, pseed, mymap, NT, 16, regs, unset_ctr, emitted);
       if (!ok) {
         const unsigned long long h = atomicAdd(heavy_count, 1ull);
         if ((int64_t)h < heavy_cap) heavy_list[h] = (u64)i;
@@ -394,17 +394,18 @@ __global__ void __launch_bounds__(NT, 4)
 // list positions).  A listed element whose first arrival lies beyond this
 // pass's tau (the list was built for tau_hi >= tau) emits that one arrival
 // and stops.
+template <class W = u32>
 __global__ void __launch_bounds__(NT)
     elem_survivor_kernel(const Surv* __restrict__ list, const unsigned long long* count, int64_t cap, u32 k,
                          u64 useed, u64 pseed, const double* __restrict__ tau_p, Reg* regs, int* unset_ctr,
                          u64* __restrict__ heavy_list, int64_t heavy_cap, unsigned long long* heavy_count,
                          unsigned long long* emitted_total) {
-  __shared__ u32 maps[16 * NT];
+  __shared__ W maps[16 * NT];
   const double tau = *tau_p;
   const double light_w = 8.0 / ((double)k * tau);
   const int64_t m = min((int64_t)*count, cap);
   u32 emitted = 0;
-  u32* mymap = maps + threadIdx.x;
+  W* mymap = maps + threadIdx.x;
   for (int64_t j = (int64_t)blockIdx.x * NT + threadIdx.x; j < m; j += (int64_t)gridDim.x * NT) {
     const Surv v = list[j];
     // the list was built for tau_hi >= tau: the filter's fp32 test against this
@@ -414,7 +415,7 @@ __global__ void __launch_bounds__(NT)
       continue;
     }
     bool ok = false;
-    if (v.w < light_w) ok = walk_light<false>(v.id, v.w, tau, k, useed, pseed, mymap, NT, 16, regs, unset_ctr, emitted);
+    if (v.w < light_w) ok = walk_light<false, W>(v.id, v.w, tau, k, useed, pseed, mymap, NT, 16, regs, unset_ctr, emitted);
     if (!ok) {
       const unsigned long long h = atomicAdd(heavy_count, 1ull);
       if ((int64_t)h < heavy_cap) heavy_list[h] = (u64)j;
@@ -432,12 +433,12 @@ __global__ void __launch_bounds__(NT)
 // the last CTA stores the registers to (y_out, s_out).
 // Heavy-list entries index the survivor list when `surv` is given (after the
 // filter), the element arrays otherwise (after the fused light kernel).
-template <class IdT, class WT>
+template <class IdT, class WT, class W = u32>
 __global__ void __launch_bounds__(NT)
     elem_heavy_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, const Surv* __restrict__ surv,
                       u32 k, u64 useed, u64 pseed, const double* __restrict__ tau_p, Reg* regs, int* unset_ctr,
                       const u64* __restrict__ heavy_list, const unsigned long long* heavy_count,
-                      int64_t heavy_cap, u32* __restrict__ dense_global,
+                      int64_t heavy_cap, W* __restrict__ dense_global,
                       unsigned long long* emitted_total, unsigned* done, double* y_out, u64* s_out) {
   __shared__ double scan_all[NWARP * 32];
   __shared__ int prov_all[NWARP * 32];
@@ -445,11 +446,11 @@ __global__ void __launch_bounds__(NT)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nh = min((int64_t)*heavy_count, heavy_cap);
   const int64_t gw = (int64_t)blockIdx.x * NWARP + warp;
-  u32* dense = dense_global + (size_t)gw * k;
+  W* dense = dense_global + (size_t)gw * k;
   u32 stamp = 0, emitted = 0;
   for (int64_t h = gw; h < nh; h += (int64_t)gridDim.x * NWARP) {
     const int64_t i = (int64_t)heavy_list[h];
-    if (++stamp == 0x10000u) {
+    if (++stamp == (FyWord<W>::BIG ? 0xFFFFFFFFu : 0x10000u)) {
       for (u32 q = lane; q < k; q += 32) dense[q] = 0;
       __syncwarp();
       stamp = 1;
@@ -620,13 +621,13 @@ __global__ void __launch_bounds__(256) weight_sample_kernel(const IdT* __restric
                                                             int64_t n, unsigned long long* table, u32 tcap, double* out,
                                                             Reg* regs, u32 k, int* unset_ctr, TauArgs targs,
                                                             unsigned* done) {
-  if (regs) {  // fresh registers (one launch fewer): the grid covers any k <= 65536
-    const u32 g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g < k) {
+  if (regs) {  // fresh registers (one launch fewer)
+    const u32 g0 = blockIdx.x * blockDim.x + threadIdx.x;
+    for (u32 g = g0; g < k; g += gridDim.x * blockDim.x) {
       regs[g].y = INF_BITS;
       regs[g].id = NO_ID;
     }
-    if (g == 0) *unset_ctr = (int)k;
+    if (g0 == 0) *unset_ctr = (int)k;
   }
   const int64_t lo = (int64_t)blockIdx.x * n / gridDim.x;
   const int64_t hi = min(lo + (int64_t)SAMPLE_RUN, ((int64_t)blockIdx.x + 1) * n / gridDim.x);
@@ -886,7 +887,7 @@ __global__ void queue_advance_kernel(const u64* __restrict__ elems, const double
     const u32 z = (u32)z0[i] + (u32)q + 1u;
     const double L = -log_pos(u_open(mix64(ubase + (u64)z * K_STEP)));
     b = __dadd_rn(b, __ddiv_rn(L, __dmul_rn(w[i], (double)(k - z + 1))));
-    const u32 jpos = perm_draw(pbase, z, k) - 1;
+    const u32 jpos = (k > 65536u ? perm_draw_big(pbase, z, k) : perm_draw(pbase, z, k)) - 1;
     const u32 vz = P[z - 1];
     P[z - 1] = P[jpos];
     P[jpos] = vz;

@@ -19,6 +19,8 @@
 //    provider chains (see walk_warp).
 #pragma once
 
+#include <type_traits>
+
 #include "gm_core.cuh"
 
 namespace gmk {
@@ -32,10 +34,12 @@ struct WalkStats {
 // (pos << 16) | (val - 1).  Returns false if the list overflowed (the caller
 // re-walks the element with the warp walker; registers already updated
 // stay valid).
-template <bool kSharedRegs>
+template <bool kSharedRegs, class W = u32>
 __device__ __forceinline__ bool walk_light(u64 id, double w, double tau, u32 k, u64 useed,
-                                           u64 pseed, u32* map, int stride, int cap, Reg* regs,
+                                           u64 pseed, W* map, int stride, int cap, Reg* regs,
                                            int* unset_ctr, u32& emitted) {
+  constexpr int SH = FyWord<W>::SH;
+  constexpr W LOW = FyWord<W>::LOW;
   const u64 ubase = useed + id * K_ELEM;
   const u64 pbase = pseed + id * K_ELEM;
   const bool fast = w_fast(w);  // the branch-free divide gives the IEEE quotient in this range
@@ -47,25 +51,25 @@ __device__ __forceinline__ bool walk_light(u64 id, double w, double tau, u32 k, 
     const double t = __dadd_rn(b, fast ? spacing_t<true>(ubase, z, w, k) : spacing_t<false>(ubase, z, w, k));
     if (t > tau) break;
     b = t;
-    const u32 j = perm_draw(pbase, z, k);
+    const u32 j = perm_draw_w<W>(pbase, z, k);
     const u32 zi = z - 1, ji = j - 1;
     u32 vz = zi + 1, vj = ji + 1;
     int sz = -1, sj = -1;
     for (int e = 0; e < nl; ++e) {
-      const u32 ent = map[e * stride];
-      const u32 p = ent >> 16;
+      const W ent = map[e * stride];
+      const u32 p = (u32)(ent >> SH);
       if (p == zi) {
-        vz = (ent & 0xFFFFu) + 1;
+        vz = (u32)(ent & LOW) + 1;
         sz = e;
       }
       if (p == ji) {
-        vj = (ent & 0xFFFFu) + 1;
+        vj = (u32)(ent & LOW) + 1;
         sj = e;
       }
     }
     // perm[zi] <- vj (dead from now on), perm[ji] <- vz
     if (ji != zi) {
-      const u32 nent = (ji << 16) | (vz - 1);
+      const W nent = ((W)ji << SH) | (W)(vz - 1);
       if (sj >= 0) {
         map[sj * stride] = nent;
         if (sz >= 0) {  // drop the dead zi entry
@@ -110,9 +114,10 @@ struct DenseStrided {  // 128-word rows, `pitch` words apart
 
 template <class D>
 __device__ __forceinline__ u32 dget(const D& dense, u32 pos, u32 stamp) {
-  if (!GM_OKIF(pos < 65536u, 20u)) return pos + 1;
-  const u32 e = dense[pos];
-  return (e >> 16) == stamp ? (e & 0xFFFFu) + 1 : pos + 1;
+  typedef std::remove_cv_t<std::remove_reference_t<decltype(dense[0])>> W;
+  if (!FyWord<W>::BIG && !GM_OKIF(pos < 65536u, 20u)) return pos + 1;
+  const W e = dense[pos];
+  return (u32)(e >> FyWord<W>::SH) == stamp ? (u32)(e & FyWord<W>::LOW) + 1 : pos + 1;
 }
 
 // One element, 32 queue steps per iteration.  Resumes at (z_start accepted
@@ -161,7 +166,9 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
     const int n_acc = stop ? __ffs(stop) - 1 : 32;
     const bool acc = lane < n_acc;
     u32 j = 0;
-    if (acc) j = (mtab && z < mtab_n) ? perm_draw_m(pbase, z, k, mtab[z]) : perm_draw(pbase, z, k);
+    typedef std::remove_cv_t<std::remove_reference_t<decltype(dense[0])>> DW;
+    if (acc) j = FyWord<DW>::BIG ? perm_draw_big(pbase, z, k)
+                 : (mtab && z < mtab_n) ? perm_draw_m(pbase, z, k, mtab[z]) : perm_draw(pbase, z, k);
     const u32 zi = z - 1, ji = j - 1;
     u32 vz = acc ? dget(dense, zi, stamp) : 0u;
     const u32 mj = acc ? dget(dense, ji, stamp) : 0u;
@@ -189,7 +196,8 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
     // positions >= z0 + n_acc stay live: last writer of each ji stores vz
     const u32 higher = same & ~((2u << lane) - 1u);
     GM_CHECK(!acc || (vj >= 1 && vj <= k && vz >= 1 && vz <= k && ji < k), 3u);
-    if (acc && higher == 0 && ji >= z0 + (u32)n_acc && GM_OKIF(ji < k, 21u)) dense[ji] = (stamp << 16) | (vz - 1);
+    if (acc && higher == 0 && ji >= z0 + (u32)n_acc && GM_OKIF(ji < k, 21u))
+      dense[ji] = ((DW)stamp << FyWord<DW>::SH) | (DW)(vz - 1);
     if (acc && GM_OKIF(vj >= 1 && vj <= k, 22u) &&
         reg_min<kSharedRegs>(&regs[vj - 1], (u64)__double_as_longlong(t), id) && unset_ctr)
       atomicSub(unset_ctr, 1);

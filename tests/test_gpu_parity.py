@@ -771,6 +771,39 @@ def test_element_queue_state_on_device_matches_reference_queues():
         assert t[i].tobytes() == to.tobytes() and s[i].tolist() == so.tolist()
 
 
+@pytest.mark.parametrize("k", [65537, 100_003, 262_144])
+def test_k_beyond_65536(k):
+    """k > 65536 (the reference accepts any k, sketch.py:139-157): the grid-wide
+    kernels with 64-bit Fisher-Yates words and exact 64-bit draws, through the
+    batch, drop-in, naive and stream entry points, against the oracle."""
+    rng = np.random.default_rng(k)
+    n = 3000
+    ids = rng.choice(1 << 40, n, replace=False).astype(np.uint64) + 1
+    w = rng.exponential(1.0, n) + 0.01
+    sc = gm.SeedScheme(k % 97)
+    order = np.argsort(ids)
+    rc, yo, so, _ = O.sketch_fast(ids[order], w[order], k, k % 97)
+    assert rc == 0
+    b = gm.sketch_csr(ids, w, np.array([0, n]), k, sc)
+    assert_regs(b.y.cpu().numpy()[0], b.s.cpu().numpy().view(np.uint64)[0], yo, so)
+    if k < 200_000:
+        v = gm.WeightedVector(dict(zip(ids[:200].tolist(), w[:200].tolist())))
+        sk = gm.sketch_fast(v, gm.GenerationParams(k=k, scheme=sc))
+        o2 = np.argsort(ids[:200])
+        rc, y2, s2, _ = O.sketch_fast(ids[:200][o2], w[:200][o2], k, k % 97)
+        assert list(sk.y) == y2.tolist() and np.array_equal(np.array(sk.s, np.uint64), s2)
+        small = gm.WeightedVector({int(e): float(x) for e, x in zip(ids[:3], w[:3])})
+        nk, em = gm.sketch_naive_counted(small, gm.GenerationParams(k=k, scheme=sc))
+        rc, y3, s3, _ = O.sketch_naive(np.sort(ids[:3]), w[:3][np.argsort(ids[:3])], k, k % 97)
+        assert list(nk.y) == y3.tolist() and np.array_equal(np.array(nk.s, np.uint64), s3) and em == 3 * k
+    rep = np.concatenate([ids, ids[:500]])
+    wr = np.concatenate([w, w[:500]])
+    y4, s4, _ = gm.sketch_elements(rep, wr, k, sc)
+    rc, y5, s5, _, _ = O.sketch_stream(rep, wr, k, k % 97)
+    assert rc == 0
+    assert_regs(y4.cpu().numpy(), s4.cpu().numpy().view(np.uint64), y5, s5)
+
+
 # ---------------------------------------------------------------- arithmetic
 def test_branch_free_divide_equals_ieee_divide():
     """ddiv_fast (the lane walkers' divide) == __ddiv_rn on its weight range."""
