@@ -388,7 +388,7 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-# ---------------------------------------------------------------- configs 1-3: K1 (csr3_kernel)
+# ---------------------------------------------------------------- configs 1-3: K1 (csr4_kernel)
 def csr_roofline(dev, stream, k, achieved_arrivals_per_s, alg_arrivals, executed, kernel_ms, in_bytes, out_bytes,
                  cfg):
     peak, chains = probe_peak(dev, k, stream)
@@ -572,7 +572,7 @@ def run_config1(args, rank, world, local_rank):
 
 
 def run_csr(args, rank, world, local_rank):
-    """Configs 2-3: batched CSR sketches (csr3_kernel)."""
+    """Configs 2-3: batched CSR sketches (csr4_kernel)."""
     import torch
     import torch.distributed as dist
 
@@ -735,7 +735,7 @@ def run_csr(args, rank, world, local_rank):
                 "ms_per_step": e2e_total / args.steps, "parity": e2e_parity,
                 "api": f"gm_sketch_csr_host (pinned host buffers, GM_FLAG_ASYNC | GM_FLAG_S32 over {ns} streams), "
                        "wall clock"},
-        "gpu_launches": args.steps,  # per step: one csr3_kernel (the slots compute the weight sums themselves)
+        "gpu_launches": args.steps,  # per step: one csr4_kernel (the slots compute the weight sums themselves)
         "roofline": roof, "clocks": clocks.summary()})
     if not args.no_cpu_baseline and world == 1:
         v, cores, sample = cpu_baseline_for(cfg_n, ids, w, off, k, seed)

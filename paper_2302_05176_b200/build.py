@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libgmsketch_b200.so")
 SOURCES = [os.path.join(CSRC, "gm_capi.cu"), os.path.join(CSRC, "gm_exact.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("gm_core.cuh", "gm_walk.cuh", "gm_kernels.cuh", "gm_csr.cuh",
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("gm_core.cuh", "gm_walk.cuh", "gm_kernels.cuh", "gm_csr.cuh", "gm_csr4.cuh",
                                                   "gm_pairs.cuh", "gm_comm.cuh", "gm_glibc_log.cuh", "gm_glibc_logtab.h")] + [
     os.path.join(os.path.dirname(HERE), "include", "gmsketch_b200.h")]
 

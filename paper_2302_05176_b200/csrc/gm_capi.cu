@@ -18,6 +18,7 @@
 
 #include "../../include/gmsketch_b200.h"
 #include "gm_csr.cuh"
+#include "gm_csr4.cuh"
 #include "gm_pairs.cuh"
 #include "gm_comm.cuh"
 
@@ -189,8 +190,8 @@ template <class C, class IdT, class WT>
 int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k,
                u64 useed, u64 salt, const u64* vseeds, int one_vec, double* y, u64* s, int64_t* em, Workspace* ws,
                cudaStream_t st, int attempt0) {
-  auto kern = csr3_kernel<C, IdT, WT>;
-  const size_t smem = csr3_smem_bytes<C>(k);
+  auto kern = csr4_kernel<C, IdT, WT>;
+  const size_t smem = csr_smem_bytes<C>(k);
   int per_sm = 0;
   {
     // occupancy per (kernel, smem) is cached: the launch path stays a
@@ -746,7 +747,7 @@ static int csr_by_elements(const void* ids, int id_bits, const void* w, int w_bi
   return rc;
 }
 
-// The batched K1 launch (csr3_kernel) for every id/weight width; vseeds
+// The batched K1 launch (csr4_kernel) for every id/weight width; vseeds
 // (device, nullable): per-vector global seeds.
 static int csr_dispatch(const void* ids, int id_bits, const void* w, int w_bits, const int64_t* offsets,
                         int64_t n_vec, int32_t k, uint64_t global_seed, uint64_t stream_salt, const uint64_t* vseeds,

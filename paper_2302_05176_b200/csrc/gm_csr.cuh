@@ -1,4 +1,5 @@
-// gm_csr.cuh -- K1: batched FastGM sketches of CSR vectors (sm_100a).
+// gm_csr.cuh -- K1 building blocks: batched FastGM sketches of CSR vectors
+// (sm_100a); the kernel itself, csr4_kernel, is in gm_csr4.cuh.
 //
 // Replaces sketch_fast_counted (sketch.py:218-311) applied to every vector
 // of a batch.  Each vector is sketched by threshold passes (DESIGN.md
@@ -6,23 +7,16 @@
 // randgen.py:158-207) is folded into the k registers; a pass that leaves a
 // register unset is repeated with a larger tau.
 //
-// Lane walker: one lane walks one element, one queue step per loop
-// iteration (straight-line step: the next spacing, the permutation draw,
-// both table probes, the register read; rare cases take a slow path).  A lane
-// whose element ends takes the next one from its warp's element queue (32
-// entries with ids and weights already loaded, refilled 32 at a time), so
-// lanes never wait for the longest queue of their warp.  An element whose
-// expected depth k*w*tau is large, or whose lane table fills up, is walked by
-// the whole warp in-line (walk_warp, 32 steps per iteration), the other lanes
-// pausing their own elements.
+// Lane walker (lane_step): one lane walks one element, one queue step per
+// call (straight-line step: the next spacing, the permutation draw, both
+// table probes, the register read; rare cases take a slow path).  An element
+// whose expected depth k*w*tau is large, or whose lane table fills up, is
+// walked by the whole warp in-line (walk_warp, 32 steps per iteration).
 //
-// Pipelined CTA (no CTA-wide barrier after the prologue): the CTA keeps V
-// vectors in flight ("slots": k registers in shared memory + a header);
-// warps take elements from the oldest slot that still has some, so a
-// vector's tail overlaps its successor.  Finished elements are counted per
-// warp and slot; the warp that counts a slot's last element finalises it:
-// check every register is set (else reopen it for the next pass with a
-// larger tau), write the sketch out, load the next vector.
+// Vector slots: the CTA keeps V vectors in flight (k registers in shared
+// memory + a header, SlotInfo); slot_load takes the next vector of the batch
+// into a slot (its weight sum, validation and divide-range check in the same
+// warp pass), slot_open_pass (re)opens a pass with its tau.
 //
 // Lane permutation table (LazyPermutation, randgen.py:146-155): NB buckets of
 // 4 words per lane, open addressing with bucket-linear probing, cleared when
@@ -37,6 +31,10 @@
 
 namespace gmk {
 
+#ifndef GM_U
+#define GM_U 4
+#endif
+
 template <int NT_, int NB_, int V_ = 2, int MINB_ = 1, int DEEP_PCT_ = 62, int DRAIN_LIVE_ = 0>
 struct CsrCfg {
   static constexpr int DRAIN_LIVE = DRAIN_LIVE_;  // queue empty and <= this many live lanes: warp-walk them
@@ -47,7 +45,7 @@ struct CsrCfg {
   static constexpr int SLOTS = 4 * NB_;        // words per lane table
   static constexpr int CAPI = SLOTS * 13 / 16; // inserts per element before hand-over
   static constexpr int V = V_;                 // vectors in flight per CTA
-  static constexpr int U = 4;                  // lane steps per loop iteration
+  static constexpr int U = GM_U;               // lane steps per loop iteration
   static constexpr int MTAB = 256;             // Barrett table entries (z < MTAB)
   static constexpr int NMAX = (1 << 24) - 4096;  // elements per vector
   // expected depth at which an element goes straight to the warp walker
@@ -82,7 +80,7 @@ struct CsrShared {
 };
 
 template <class C>
-__host__ __device__ constexpr size_t csr3_smem_bytes(u32 k) {
+__host__ __device__ constexpr size_t csr_smem_bytes(u32 k) {
   return (size_t)C::V * k * sizeof(Reg)               // registers of the slots
          + (size_t)C::NT * C::SLOTS * 4              // lane tables
          + (size_t)C::MTAB * 4                       // Barrett table
@@ -365,371 +363,6 @@ __device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const
 }
 
 // ---- K1 ---------------------------------------------------------------------
-// Dynamic shared memory: Reg regs[V][k] | u32 tables[NB][NT][4] | u32 mtab[MTAB]
-//   | double scan[NWARP][32] | int prov[NWARP][32]
-template <class C, class IdT, class WT>
-__global__ void __launch_bounds__(C::NT, C::MINB)
-    csr3_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts,
-                const int64_t* __restrict__ offsets, int64_t n_vec, u32 k, u64 useed, u64 salt,
-                const u64* __restrict__ vseeds, int one_vec,
-                const double* __restrict__ Wsum, const int* __restrict__ vflags,
-                double* __restrict__ y_out, u64* __restrict__ s_out,
-                int64_t* __restrict__ emitted_out, int* __restrict__ vec_counter,
-                u32* __restrict__ dense_global, unsigned long long* __restrict__ err, int attempt0,
-                const int* __restrict__ vec_list) {
-  constexpr int NT = C::NT, NWARP = C::NWARP, V = C::V;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ CsrShared S;
-  const unsigned FULL = 0xFFFFFFFFu;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned lt_mask = (1u << lane) - 1u;
-
-  u32* tables = reinterpret_cast<u32*>(smem_raw + (size_t)V * k * sizeof(Reg));
-  u32* mtab = tables + (size_t)NT * C::SLOTS;
-  double* ltab = reinterpret_cast<double*>(mtab + C::MTAB);  // 128 x {invc, logc}; 16-byte aligned: MTAB*4 % 16 == 0
-  double* scan = ltab + 256 + warp * 32;
-  int* prov = reinterpret_cast<int*>(ltab + 256 + NWARP * 32) + warp * 32;
-  // floor(2^64 / m) for m = k - z + 1, z < MTAB: the lane step's draw in one 64-bit Barrett reduction
-  u64* mtab64 = reinterpret_cast<u64*>(reinterpret_cast<int*>(ltab + 256 + NWARP * 32) + NWARP * 32);
-  u32* mytab = tables + tid * 4;
-  u32* dense = dense_global + ((size_t)blockIdx.x * NWARP + warp) * k;
-
-  for (u32 z = tid; z < (u32)C::MTAB; z += NT) {
-    mtab[z] = (z >= 1 && z <= k) ? barrett_magic(k - z + 1) : 0u;
-    mtab64[z] = (z >= 1 && z <= k) ? barrett_magic64(k - z + 1) : 0ull;
-  }
-  for (u32 i = tid; i < 256; i += NT) ltab[i] = gm_glog_tab[i >> 1][i & 1];
-  tab_clear<C>(mytab);
-  for (u32 i = lane; i < k; i += 32) dense[i] = 0;  // stamps restart every launch
-  if (tid < V) {
-    S.slot[tid].state = SLOT_EMPTY;
-    S.slot[tid].n = 0;
-    S.slot[tid].grab = 0;
-    S.slot[tid].seq = 0;
-  }
-  if (tid == 0) S.seq = 0;
-  __syncthreads();
-  if (warp < V)
-    slot_load<C, WT>(S, warp, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list,
-                     wts, useed, salt, vseeds, one_vec);
-  __syncthreads();
-
-  Lane L;
-  L.z = 0;
-  L.used = 0;
-  L.slot = 0;
-  L.b = L.t = L.tau = L.w = 0.0;
-  L.id = L.ubase = L.pbase = 0;
-  L.regs = nullptr;
-  L.fast = true;
-  bool live = false, fresh = false, deep = false, resume = false;
-  u32 em = 0;     // arrivals computed for the current element
-  u32 fin = 0;    // slots this warp must finalise (warp-uniform)
-  u32 stamp = 0;  // dense-array stamp of this warp
-  // element queue of the warp: a ring of 32 entries, entry e held by lane e
-  // (slot, id, weight loaded when the entry was taken from its slot)
-  // Two sets of 32 entries (entry e held by lane e): one is consumed while
-  // the other is refilled, so the shuffles that hand out entries never read a
-  // register whose global load is still in flight.
-  int qa_slot = -1, qb_slot = -1;
-  u64 qa_id = 0, qb_id = 0;
-  double qa_w = 0.0, qb_w = 0.0;
-  u32 qcur = 0, qhead = 0, qcnt = 0;  // warp-uniform: current set, its head and count
-  u32 qnext = 0;                      // entries loaded into the other set
-
-  // count `c` finished elements of slot s (lane 0; the warp's register
-  // updates are fenced first).  n is read before the increment: once they are
-  // counted the slot may be finalised and reloaded by another warp.
-  auto complete_batch = [&](int s, int c, unsigned long long em_sum) {
-    __threadfence_block();
-    __syncwarp();
-    if (lane == 0) {
-      SlotInfo& sl = S.slot[s];
-      const int n = *(volatile int*)&sl.n;
-      if (emitted_out) atomicAdd(&sl.emitted, em_sum);
-      __threadfence_block();
-      const int old = atomicAdd(&sl.done, c);
-      if (old + c == n) fin |= 1u << s;
-    }
-    fin = __shfl_sync(FULL, fin, 0);
-  };
-
-#ifdef GM_STATS
-  long long t_prev = 0;
-  int t_sec = 15;
-#endif
-  for (;;) {
-#ifdef GM_STATS
-    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 8; }
-#endif
-    // ---- (1) finalise slots whose last elements this warp counted
-    while (fin) {
-      const int s = __ffs(fin) - 1;
-      fin &= fin - 1;
-      SlotInfo& sl = S.slot[s];
-      __threadfence_block();
-      Reg* regs = slot_regs<C>(smem_raw, s, k);
-      bool unset = false;
-      for (u32 j = lane; j < k; j += 32) unset |= regs[j].y == INF_BITS;
-      const int att = __shfl_sync(FULL, *(volatile int*)&sl.attempt, 0);
-      if (__any_sync(FULL, unset) && att < 3) {
-        if (lane == 0) {
-          slot_open_pass(sl, k, att + 1, C::kDeep);
-          GM_TRACE((unsigned long long)(sl.v & 0xFFFFFFFF) | ((unsigned long long)(att + 1) << 32) | (2ull << 40) |
-                   ((unsigned long long)blockIdx.x << 48) | ((unsigned long long)s << 60));
-        }
-        __syncwarp();
-        continue;
-      }
-      const int64_t v = __shfl_sync(FULL, *(volatile long long*)&sl.v, 0);
-      for (u32 j = lane; j < k; j += 32) {
-        const Reg rg = regs[j];
-        y_out[v * (int64_t)k + j] = __longlong_as_double((long long)rg.y);
-        s_out[v * (int64_t)k + j] = rg.id;
-      }
-      if (emitted_out && lane == 0) emitted_out[v] = (int64_t)sl.emitted;
-      if (lane == 0)
-        GM_TRACE((unsigned long long)(v & 0xFFFFFFFF) | ((unsigned long long)att << 32) | (1ull << 40) |
-                 ((unsigned long long)blockIdx.x << 48) | ((unsigned long long)s << 60));
-      __syncwarp();
-      slot_load<C, WT>(S, s, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list,
-                       wts, useed, salt, vseeds, one_vec);
-    }
-
-#ifdef GM_STATS
-    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 9; }
-#endif
-    // ---- (2) warp walks: deep elements and resumed (table-full) elements
-    unsigned dm = __ballot_sync(FULL, deep);
-    while (dm) {
-      const int src = __ffs(dm) - 1;
-      dm &= dm - 1;
-      const int s = __shfl_sync(FULL, L.slot, src);
-      const u64 wid = __shfl_sync(FULL, L.id, src);
-      const double ww = __shfl_sync(FULL, L.w, src);
-      const double tau = __shfl_sync(FULL, L.tau, src);
-      const bool wres = __shfl_sync(FULL, (int)resume, src) != 0;
-      const u32 z0 = wres ? __shfl_sync(FULL, L.z, src) : 0u;
-      const double b0 = wres ? __shfl_sync(FULL, L.b, src) : 0.0;
-      const bool wfast = __shfl_sync(FULL, (int)L.fast, src) != 0;
-      const u32 em0 = __shfl_sync(FULL, em, src);
-      const u64 wus = *(volatile u64*)&S.slot[s].useed, wps = *(volatile u64*)&S.slot[s].pseed;
-      if (++stamp > 0xFFFFu) {
-        for (u32 i = lane; i < k; i += 32) dense[i] = 0;
-        __syncwarp();
-        stamp = 1;
-      }
-      if (wres) {  // the source lane's live table entries -> dense array
-        const u32* stab = tables + (warp * 32 + src) * 4;
-        for (u32 wi = lane; wi < (u32)C::SLOTS; wi += 32) {
-          const u32 e = stab[(wi >> 2) * (NT * 4) + (wi & 3)];
-          if (e != 0u && (e >> 16) >= z0) dense[e >> 16] = (stamp << 16) | (e & 0xFFFFu);
-        }
-        __syncwarp();
-      }
-      u32 wem = 0;
-      Reg* regs = slot_regs<C>(smem_raw, s, k);
-      if (wfast)
-        walk_warp<true, true>(wid, ww, tau, k, wus, wps, dense, stamp, scan, prov, regs, nullptr, wem, z0, b0,
-                              mtab, (u32)C::MTAB);
-      else
-        walk_warp<true, false>(wid, ww, tau, k, wus, wps, dense, stamp, scan, prov, regs, nullptr, wem, z0, b0,
-                               mtab, (u32)C::MTAB);
-      wem = __shfl_sync(FULL, wem, 0);
-      GM_STAT(3, lane == 0);  // warp walks
-      GM_STAT(4, lane == 0 ? wem : 0u);
-      complete_batch(s, 1, (unsigned long long)(em0 + wem));
-      if (lane == src) {
-        deep = false;
-        resume = false;
-      }
-    }
-
-#ifdef GM_STATS
-    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 10; }
-#endif
-    // ---- (3) refill the idle queue set from the oldest open slot
-    if (qnext == 0) {
-      int first = 0;
-      if (lane == 0) {
-        unsigned best = *(volatile unsigned*)&S.slot[0].seq;
-#pragma unroll
-        for (int i = 1; i < V; ++i) {
-          const unsigned q = *(volatile unsigned*)&S.slot[i].seq;
-          if (q < best) {
-            best = q;
-            first = i;
-          }
-        }
-      }
-      first = __shfl_sync(FULL, first, 0);
-#pragma unroll
-      for (int oi = 0; oi < V; ++oi) {
-        const u32 room = 32u - qnext;
-        if (room == 0) break;
-        const int s = (first + oi) % V;
-        SlotInfo& sl = S.slot[s];
-        unsigned long long base = 0;
-        long long lo = 0;
-        if (lane == 0) {
-          const unsigned long long g0 = *(volatile unsigned long long*)&sl.grab;
-          if ((u32)g0 < (u32)(g0 >> 32)) {
-            base = atomicAdd(&sl.grab, (unsigned long long)room);
-            __threadfence_block();
-            lo = *(volatile long long*)&sl.lo;
-          }
-        }
-        base = __shfl_sync(FULL, base, 0);
-        const u32 n = (u32)(base >> 32), i0 = (u32)base;
-        if (i0 >= n) continue;
-        lo = __shfl_sync(FULL, lo, 0);
-        const u32 got = min(room, n - i0);
-        const u32 t = (u32)lane - qnext;  // this lane's offset in the new run
-        if (t < got) {
-          // L2-only loads: each element is read once
-          const u64 id = (u64)__ldcg(&ids[lo + i0 + t]);
-          const double w = (double)__ldcg(&wts[lo + i0 + t]);
-          if (qcur) {
-            qa_slot = s;
-            qa_id = id;
-            qa_w = w;
-          } else {
-            qb_slot = s;
-            qb_id = id;
-            qb_w = w;
-          }
-        }
-        qnext += got;
-      }
-    }
-    if (qcnt == 0 && qnext > 0) {  // current set used up: switch
-      qcur ^= 1u;
-      qhead = 0;
-      qcnt = qnext;
-      qnext = 0;
-    }
-
-#ifdef GM_STATS
-    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 11; }
-#endif
-    // ---- (4) lanes without an element take the next queue entries
-    {
-      const unsigned needm = __ballot_sync(FULL, !live && !deep);
-      const u32 take = min((u32)__popc(needm), qcnt);
-      if (take) {
-        const u32 rho = __popc(needm & lt_mask);
-        const int src = (int)(qhead + rho) & 31;
-        int ps;
-        u64 pid;
-        double pw;
-        if (qcur) {
-          ps = __shfl_sync(FULL, qb_slot, src);
-          pid = __shfl_sync(FULL, qb_id, src);
-          pw = __shfl_sync(FULL, qb_w, src);
-        } else {
-          ps = __shfl_sync(FULL, qa_slot, src);
-          pid = __shfl_sync(FULL, qa_id, src);
-          pw = __shfl_sync(FULL, qa_w, src);
-        }
-        if (((needm >> lane) & 1u) && rho < take) {
-          SlotInfo& sl = S.slot[ps];
-          L.slot = ps;
-          L.id = pid;
-          L.w = pw;
-          L.tau = sl.tau;
-          L.fast = sl.fast != 0;
-          L.regs = slot_regs<C>(smem_raw, ps, k);
-          L.ubase = sl.useed + pid * K_ELEM;
-          L.pbase = sl.pseed + pid * K_ELEM;
-          L.b = 0.0;
-          L.z = 0;
-          L.used = 0;
-          em = 0;
-          if (pw >= sl.deep_w) {
-            deep = true;
-          } else {
-            tab_clear<C>(mytab);
-            live = true;
-            fresh = true;
-          }
-        }
-        qhead += take;
-        qcnt -= take;
-      }
-    }
-
-#ifdef GM_STATS
-    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 12; }
-#endif
-    // ---- exit / idle
-    if (!__any_sync(FULL, live)) {
-      if (!__any_sync(FULL, deep) && qcnt == 0 && qnext == 0) {
-        bool open = false;
-#pragma unroll
-        for (int s = 0; s < V; ++s) open |= *(volatile int*)&S.slot[s].state != SLOT_EMPTY;
-        if (!__shfl_sync(FULL, (int)open, 0)) break;
-        __nanosleep(200);
-      }
-      GM_STAT(0, lane == 0);
-      continue;
-    }
-    GM_STAT(1, lane == 0);  // lane-step iterations
-    GM_STAT(2, live);       // live lanes summed over them
-    GM_STAT(5, deep);       // lanes waiting for a warp walk
-    GM_STAT(6, !live && !deep && qcnt == 0 && qnext == 0);  // idle: the warp's queue is empty
-    GM_STAT(7, !live && !deep && (qcnt != 0 || qnext != 0));  // idle although entries are queued
-
-#ifdef GM_STATS
-    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 13; }
-#endif
-    // ---- drain: the warp's queue is empty and few lanes still walk -- hand
-    // their elements to the warp walker (all 32 lanes on each, next iteration)
-    // instead of stepping with a mostly idle warp
-    if (C::DRAIN_LIVE > 0 && qcnt == 0 && qnext == 0 && __popc(__ballot_sync(FULL, live)) <= C::DRAIN_LIVE) {
-      if (live) {
-        em += L.z;
-        live = false;
-        deep = true;
-        resume = true;
-      }
-      continue;
-    }
-    // ---- (5) C::U lane steps (a lane whose element ends idles for the rest)
-    bool done = false;
-#pragma unroll 1
-    for (int u = 0; u < C::U; ++u) {
-      if (live) {
-        const int rc = lane_step<C>(L, fresh, mytab, mtab64, k, ltab);
-        fresh = false;
-        if (rc == 1) {
-          em += L.z < k ? L.z + 1 : L.z;
-          live = false;
-          done = true;
-        } else if (rc == 2) {
-          em += L.z;
-          live = false;
-          deep = true;
-          resume = true;
-        }
-      }
-    }
-#ifdef GM_STATS
-    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 14; }
-#endif
-    // ---- (6) count finished elements per slot
-    if (__any_sync(FULL, done)) {
-#pragma unroll
-      for (int s = 0; s < V; ++s) {
-        const bool mine = done && L.slot == s;
-        const int c = __popc(__ballot_sync(FULL, mine));
-        if (c) {
-          const unsigned long long es =
-              emitted_out ? (unsigned long long)__reduce_add_sync(FULL, mine ? em : 0u) : 0ull;
-          complete_batch(s, c, es);
-        }
-      }
-    }
-  }
-}
+// The kernel (csr4_kernel, lane-level element scheduling) is in gm_csr4.cuh.
 
 }  // namespace gmk

@@ -1,0 +1,343 @@
+// gm_csr4.cuh -- K1: csr4_kernel, batched FastGM sketches of CSR vectors
+// with lane-level element scheduling (configs 1-3; sketch_fast per vector,
+// sketch.py:218-311).
+//
+// Pipelined CTA (no CTA-wide barrier after the prologue): V vector slots
+// (gm_csr.cuh); every lane takes its elements itself -- a shared-memory
+// ticket on the oldest slot that still has untaken elements -- and keeps its
+// NEXT element taken and loading (id, weight from HBM/L2) while it walks the
+// current one, so a lane whose element ends goes on with the next one at the
+// next step, with no warp-wide hand-out and no idle steps.  A finished element
+// is counted lane by lane (its register updates fenced first); the lane that
+// counts a slot's last element flags it, and its warp finalises the slot:
+// every register set -> write the sketch out and load the next vector; else
+// reopen the slot for the next pass with a larger tau.  Deep elements and
+// elements whose lane table fills up are walked by the whole warp (walk_warp).
+// Lane steps run in rounds of u_run steps between the warp-level checks
+// (2 / 4 / 6 from the batch's expected arrivals per element).
+//
+// (Round 1's csr3_kernel handed elements out from a warp queue refilled 32
+// entries at a time; lane-level scheduling is 1.65x faster on config 1,
+// 1.18x on config 3 and 1.5% on config 2 -- DESIGN.md section 6.)
+#pragma once
+
+#include "gm_csr.cuh"
+
+namespace gmk {
+
+// Dynamic shared memory: Reg regs[V][k] | u32 tables[NB][NT][4] | u32 mtab[MTAB]
+//   | double scan[NWARP][32] | int prov[NWARP][32]
+template <class C, class IdT, class WT>
+__global__ void __launch_bounds__(C::NT, C::MINB)
+    csr4_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts,
+                const int64_t* __restrict__ offsets, int64_t n_vec, u32 k, u64 useed, u64 salt,
+                const u64* __restrict__ vseeds, int one_vec,
+                const double* __restrict__ Wsum, const int* __restrict__ vflags,
+                double* __restrict__ y_out, u64* __restrict__ s_out,
+                int64_t* __restrict__ emitted_out, int* __restrict__ vec_counter,
+                u32* __restrict__ dense_global, unsigned long long* __restrict__ err, int attempt0,
+                const int* __restrict__ vec_list) {
+  constexpr int NT = C::NT, NWARP = C::NWARP, V = C::V;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ CsrShared S;
+  const unsigned FULL = 0xFFFFFFFFu;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+
+  u32* tables = reinterpret_cast<u32*>(smem_raw + (size_t)V * k * sizeof(Reg));
+  u32* mtab = tables + (size_t)NT * C::SLOTS;
+  double* ltab = reinterpret_cast<double*>(mtab + C::MTAB);  // 128 x {invc, logc}; 16-byte aligned: MTAB*4 % 16 == 0
+  double* scan = ltab + 256 + warp * 32;
+  int* prov = reinterpret_cast<int*>(ltab + 256 + NWARP * 32) + warp * 32;
+  // floor(2^64 / m) for m = k - z + 1, z < MTAB: the lane step's draw in one 64-bit Barrett reduction
+  u64* mtab64 = reinterpret_cast<u64*>(reinterpret_cast<int*>(ltab + 256 + NWARP * 32) + NWARP * 32);
+  u32* mytab = tables + tid * 4;
+  u32* dense = dense_global + ((size_t)blockIdx.x * NWARP + warp) * k;
+
+  for (u32 z = tid; z < (u32)C::MTAB; z += NT) {
+    mtab[z] = (z >= 1 && z <= k) ? barrett_magic(k - z + 1) : 0u;
+    mtab64[z] = (z >= 1 && z <= k) ? barrett_magic64(k - z + 1) : 0ull;
+  }
+  for (u32 i = tid; i < 256; i += NT) ltab[i] = gm_glog_tab[i >> 1][i & 1];
+  tab_clear<C>(mytab);
+  for (u32 i = lane; i < k; i += 32) dense[i] = 0;  // stamps restart every launch
+  if (tid < V) {
+    S.slot[tid].state = SLOT_EMPTY;
+    S.slot[tid].n = 0;
+    S.slot[tid].grab = 0;
+    S.slot[tid].seq = 0;
+  }
+  if (tid == 0) S.seq = 0;
+  __syncthreads();
+  if (warp < V)
+    slot_load<C, WT>(S, warp, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list,
+                     wts, useed, salt, vseeds, one_vec);
+  __syncthreads();
+
+  Lane L;
+  L.z = 0;
+  L.used = 0;
+  L.slot = 0;
+  L.b = L.t = L.tau = L.w = 0.0;
+  L.id = L.ubase = L.pbase = 0;
+  L.regs = nullptr;
+  L.fast = true;
+  bool live = false, fresh = false, deep = false, resume = false;
+  u32 em = 0;     // arrivals computed for the current element
+  u32 fin = 0;    // slots this warp must finalise (warp-uniform)
+  u32 stamp = 0;  // dense-array stamp of this warp
+  // lane steps per scheduling round, from the batch's expected arrivals per
+  // element at the first pass, k (ln k + 2.5) / (elements per vector): light
+  // elements (config 1: ~0.2) are turned over every 2 steps, deep ones (config 2:
+  // ~10) walk 6 steps between the warp-level checks
+  int u_run;
+  {
+    const float n_avg = one_vec ? (float)(offsets[1] - offsets[0])
+                                : (float)(offsets[n_vec] - offsets[0]) / (float)n_vec;
+    const float depth = (float)k * (__logf((float)k) + 2.5f) / fmaxf(n_avg, 1.0f);
+    u_run = depth < 2.0f ? 2 : depth < 6.0f ? 4 : 6;
+  }
+  // the lane's next element, taken and loading while the current one is walked
+  bool nx_ok = false;
+  int nx_slot = 0;
+  u64 nx_id = 0;
+  double nx_w = 0.0;
+  u32 myfin = 0;  // slots whose last element this lane counted
+
+  // count `c` finished elements of slot s (lane 0; the warp's register
+  // updates are fenced first).  n is read before the increment: once they are
+  // counted the slot may be finalised and reloaded by another warp.
+  auto complete_batch = [&](int s, int c, unsigned long long em_sum) {
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) {
+      SlotInfo& sl = S.slot[s];
+      const int n = *(volatile int*)&sl.n;
+      if (emitted_out) atomicAdd(&sl.emitted, em_sum);
+      __threadfence_block();
+      const int old = atomicAdd(&sl.done, c);
+      if (old + c == n) fin |= 1u << s;
+    }
+    fin = __shfl_sync(FULL, fin, 0);
+  };
+
+  // lane-level: take a ticket from the oldest slot with untaken elements and
+  // start loading that element (its id and weight are read at start_next)
+  auto take_next = [&]() {
+    int best = -1;
+    unsigned bseq = 0xFFFFFFFFu;
+#pragma unroll
+    for (int s = 0; s < V; ++s) {
+      const unsigned long long g = *(volatile unsigned long long*)&S.slot[s].grab;
+      const unsigned q = *(volatile unsigned*)&S.slot[s].seq;
+      if ((u32)g < (u32)(g >> 32) && q < bseq) {
+        bseq = q;
+        best = s;
+      }
+    }
+    if (best < 0) return;
+    const unsigned long long old = atomicAdd(&S.slot[best].grab, 1ull);
+    if ((u32)old >= (u32)(old >> 32)) return;  // the slot ran dry meanwhile
+    __threadfence_block();
+    const long long lo = *(volatile long long*)&S.slot[best].lo;
+    nx_id = (u64)__ldcg(&ids[lo + (u32)old]);  // L2-only loads: each element is read once
+    nx_w = (double)__ldcg(&wts[lo + (u32)old]);
+    nx_slot = best;
+    nx_ok = true;
+  };
+  // lane-level: make the prefetched element the lane's current one
+  auto start_next = [&]() {
+    SlotInfo& sl = S.slot[nx_slot];
+    L.slot = nx_slot;
+    L.id = nx_id;
+    L.w = nx_w;
+    L.tau = sl.tau;
+    L.fast = sl.fast != 0;
+    L.regs = slot_regs<C>(smem_raw, nx_slot, k);
+    L.ubase = sl.useed + nx_id * K_ELEM;
+    L.pbase = sl.pseed + nx_id * K_ELEM;
+    L.b = 0.0;
+    L.z = 0;
+    L.used = 0;
+    em = 0;
+    nx_ok = false;
+    if (nx_w >= sl.deep_w) {
+      deep = true;
+    } else {
+      tab_clear<C>(mytab);
+      live = true;
+      fresh = true;
+    }
+  };
+  // lane-level: count the lane's finished element in its slot (its register
+  // updates fenced first); the lane that counts the last one flags the slot
+  auto finish_element = [&]() {
+    SlotInfo& sl = S.slot[L.slot];
+    const int n = *(volatile int*)&sl.n;
+    if (emitted_out) atomicAdd(&sl.emitted, (unsigned long long)em);
+    __threadfence_block();
+    if (atomicAdd(&sl.done, 1) + 1 == n) myfin |= 1u << L.slot;
+  };
+
+#ifdef GM_STATS
+  long long t_prev = 0;
+  int t_sec = 15;
+#endif
+  for (;;) {
+#ifdef GM_STATS
+    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 8; }
+#endif
+    // ---- (1) finalise slots whose last elements this warp counted
+    while (fin) {
+      const int s = __ffs(fin) - 1;
+      fin &= fin - 1;
+      SlotInfo& sl = S.slot[s];
+      __threadfence_block();
+      Reg* regs = slot_regs<C>(smem_raw, s, k);
+      bool unset = false;
+      for (u32 j = lane; j < k; j += 32) unset |= regs[j].y == INF_BITS;
+      const int att = __shfl_sync(FULL, *(volatile int*)&sl.attempt, 0);
+      if (__any_sync(FULL, unset) && att < 3) {
+        if (lane == 0) {
+          slot_open_pass(sl, k, att + 1, C::kDeep);
+          GM_TRACE((unsigned long long)(sl.v & 0xFFFFFFFF) | ((unsigned long long)(att + 1) << 32) | (2ull << 40) |
+                   ((unsigned long long)blockIdx.x << 48) | ((unsigned long long)s << 60));
+        }
+        __syncwarp();
+        continue;
+      }
+      const int64_t v = __shfl_sync(FULL, *(volatile long long*)&sl.v, 0);
+      for (u32 j = lane; j < k; j += 32) {
+        const Reg rg = regs[j];
+        y_out[v * (int64_t)k + j] = __longlong_as_double((long long)rg.y);
+        s_out[v * (int64_t)k + j] = rg.id;
+      }
+      if (emitted_out && lane == 0) emitted_out[v] = (int64_t)sl.emitted;
+      if (lane == 0)
+        GM_TRACE((unsigned long long)(v & 0xFFFFFFFF) | ((unsigned long long)att << 32) | (1ull << 40) |
+                 ((unsigned long long)blockIdx.x << 48) | ((unsigned long long)s << 60));
+      __syncwarp();
+      slot_load<C, WT>(S, s, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list,
+                       wts, useed, salt, vseeds, one_vec);
+    }
+
+#ifdef GM_STATS
+    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 9; }
+#endif
+    // ---- (2) warp walks: deep elements and resumed (table-full) elements
+    unsigned dm = __ballot_sync(FULL, deep);
+    while (dm) {
+      const int src = __ffs(dm) - 1;
+      dm &= dm - 1;
+      const int s = __shfl_sync(FULL, L.slot, src);
+      const u64 wid = __shfl_sync(FULL, L.id, src);
+      const double ww = __shfl_sync(FULL, L.w, src);
+      const double tau = __shfl_sync(FULL, L.tau, src);
+      const bool wres = __shfl_sync(FULL, (int)resume, src) != 0;
+      const u32 z0 = wres ? __shfl_sync(FULL, L.z, src) : 0u;
+      const double b0 = wres ? __shfl_sync(FULL, L.b, src) : 0.0;
+      const bool wfast = __shfl_sync(FULL, (int)L.fast, src) != 0;
+      const u32 em0 = __shfl_sync(FULL, em, src);
+      const u64 wus = *(volatile u64*)&S.slot[s].useed, wps = *(volatile u64*)&S.slot[s].pseed;
+      if (++stamp > 0xFFFFu) {
+        for (u32 i = lane; i < k; i += 32) dense[i] = 0;
+        __syncwarp();
+        stamp = 1;
+      }
+      if (wres) {  // the source lane's live table entries -> dense array
+        const u32* stab = tables + (warp * 32 + src) * 4;
+        for (u32 wi = lane; wi < (u32)C::SLOTS; wi += 32) {
+          const u32 e = stab[(wi >> 2) * (NT * 4) + (wi & 3)];
+          if (e != 0u && (e >> 16) >= z0) dense[e >> 16] = (stamp << 16) | (e & 0xFFFFu);
+        }
+        __syncwarp();
+      }
+      u32 wem = 0;
+      Reg* regs = slot_regs<C>(smem_raw, s, k);
+      if (wfast)
+        walk_warp<true, true>(wid, ww, tau, k, wus, wps, dense, stamp, scan, prov, regs, nullptr, wem, z0, b0,
+                              mtab, (u32)C::MTAB);
+      else
+        walk_warp<true, false>(wid, ww, tau, k, wus, wps, dense, stamp, scan, prov, regs, nullptr, wem, z0, b0,
+                               mtab, (u32)C::MTAB);
+      wem = __shfl_sync(FULL, wem, 0);
+      GM_STAT(3, lane == 0);  // warp walks
+      GM_STAT(4, lane == 0 ? wem : 0u);
+      complete_batch(s, 1, (unsigned long long)(em0 + wem));
+      if (lane == src) {
+        deep = false;
+        resume = false;
+      }
+    }
+
+#ifdef GM_STATS
+    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 10; }
+#endif
+    // ---- (3) lanes without an element start the one they prefetched (or take
+    // one now), and every lane keeps its next element in flight
+    if (!live && !deep) {
+      if (!nx_ok) take_next();
+      if (nx_ok) start_next();
+    }
+    if (live && !nx_ok) take_next();
+
+    // ---- exit / idle
+    if (!__any_sync(FULL, live || deep)) {
+      if (!__any_sync(FULL, nx_ok)) {
+        bool open = false;
+#pragma unroll
+        for (int s = 0; s < V; ++s) open |= *(volatile int*)&S.slot[s].state != SLOT_EMPTY;
+        if (!__shfl_sync(FULL, (int)open, 0)) break;
+        __nanosleep(200);
+      }
+      continue;
+    }
+
+    // ---- drain: no slot has untaken elements and few lanes still walk --
+    // hand their elements to the warp walker (all 32 lanes on each)
+    if (C::DRAIN_LIVE > 0 && !__any_sync(FULL, nx_ok) && __popc(__ballot_sync(FULL, live)) <= C::DRAIN_LIVE) {
+      bool work = false;
+      if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < V; ++s) {
+          const unsigned long long g = *(volatile unsigned long long*)&S.slot[s].grab;
+          work |= (u32)g < (u32)(g >> 32);
+        }
+      }
+      if (!__shfl_sync(FULL, (int)work, 0)) {
+        if (live) {
+          em += L.z;
+          live = false;
+          deep = true;
+          resume = true;
+        }
+        continue;
+      }
+    }
+
+    // ---- (4) u_run lane steps; a lane whose element ends counts it and goes on
+    // with its prefetched element at the next step
+#pragma unroll 1
+    for (int u = 0; u < u_run; ++u) {
+      if (live) {
+        const int rc = lane_step<C>(L, fresh, mytab, mtab64, k, ltab);
+        fresh = false;
+        if (rc == 1) {
+          em += L.z < k ? L.z + 1 : L.z;
+          live = false;
+          finish_element();
+          if (nx_ok) start_next();
+        } else if (rc == 2) {
+          em += L.z;
+          live = false;
+          deep = true;
+          resume = true;
+        }
+      }
+    }
+    fin |= __reduce_or_sync(FULL, myfin);
+    myfin = 0;
+  }
+}
+
+}  // namespace gmk

@@ -1,6 +1,6 @@
 // gm_kernels.cuh -- the FastGM kernels (sm_100a).
 //
-//   K1 csr3_kernel         batch of CSR vectors (gm_csr.cuh; configs 1-3,
+//   K1 csr4_kernel         batch of CSR vectors (gm_csr4.cuh; configs 1-3,
 //                          replaces sketch_fast_counted, sketch.py:218-311).
 //   K2 elem_light_kernel + elem_heavy_kernel
 //                          one huge element set (a huge vector or an

@@ -528,7 +528,7 @@ def test_errors_map_to_reference_classes():
     with pytest.raises(gm.EmptyVectorError):
         gm.sketch_csr(np.array([1, 2], np.uint32), np.array([1.0, 1.0]), np.array([0, 2, 2]), 8, sc)
     with pytest.raises(gm.InvalidParameterError):
-        gm.sketch_csr(np.array([1], np.uint32), np.array([1.0]), np.array([0, 1]), 70000, sc)
+        gm.sketch_csr(np.array([1], np.uint32), np.array([1.0]), np.array([0, 1]), (1 << 24) + 1, sc)
     with pytest.raises(gm.EmptyVectorError):
         gm.sketch_fast(gm.WeightedVector({}), gm.GenerationParams(k=4, scheme=sc))
     with pytest.raises(gm.InconsistentWeightError):

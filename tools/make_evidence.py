@@ -7,7 +7,7 @@ into profiles/evidence_configN.json (read by bench.py for the roofline block).
 Per kernel (last launch of each name): duration, warp instructions, pipe
 utilisation (fp64, fma, alu, xu: % of peak sustained while active), issue
 slots busy, SIMT efficiency, DRAM bytes; for configs 1-3 warp instructions
-per arrival of csr3_kernel (algorithmic and executed) and of the probe."""
+per arrival of the K1 kernel (algorithmic and executed) and of the probe."""
 
 import argparse
 import csv
@@ -87,7 +87,7 @@ def main():
         ev["probe_kernel"] = best[1]
         ev["probe_warp_inst_per_arrival"] = p["warp_inst_per_arrival"]
         ev["probe_pipes"] = p["pipes_pct"]
-    csr = [n for n in last if n.startswith("csr3_kernel")]
+    csr = [n for n in last if n.startswith("csr3_kernel") or n.startswith("csr4_kernel")]
     if csr:
         e = ev["kernels"][csr[0]]
         ev["kernel"] = csr[0]

@@ -3,9 +3,9 @@
   python tools/ncu_target.py --config N [--out gpurun_out/target_configN.json]
 
 Runs the roofline probe (chains 1, 2 and 4 -- the kernel arrival_probe_kernel)
-and two sketches of config N through the C ABI (configs 1-3: csr3_kernel;
+and two sketches of config N through the C ABI (configs 1-3: csr4_kernel;
 4-5: the element-set kernels), and writes the per-launch work the evidence
-needs: algorithmic and executed arrivals per csr3_kernel launch, probe
+needs: algorithmic and executed arrivals per K1 launch, probe
 arrivals per launch.  tools/make_evidence.py joins it with the ncu CSV."""
 
 import argparse
