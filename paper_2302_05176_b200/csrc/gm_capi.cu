@@ -180,11 +180,23 @@ int num_sms() {
 #ifndef GM_DRAIN
 #define GM_DRAIN 4
 #endif
-using CsrDefault = CsrCfg<256, 16, 2, 2, GM_DEEP_PCT, GM_DRAIN>;
+#ifndef GM_NB
+#define GM_NB 16  // lane-table buckets (4 words each)
+#endif
+#ifndef GM_MINB
+#define GM_MINB 2  // resident CTAs per SM the register budget is sized for
+#endif
+#ifndef GM_VSMALL
+#define GM_VSMALL 4
+#endif
+// k <= 4096: 12-bit lane-table words with a generation tag (no table clear
+// per element); larger k: 16-bit words, cleared per element
+using CsrDefault = CsrCfg<256, GM_NB, 2, GM_MINB, GM_DEEP_PCT, GM_DRAIN, 12>;
+using CsrLargeK = CsrCfg<256, 16, 2, 2, GM_DEEP_PCT, GM_DRAIN, 16>;
 // k <= 512: four vector slots fit in the shared memory two slots of k = 1024
 // take, so a CTA keeps four (small) vectors in flight -- fewer lanes idle
 // while a slot drains (config 3: 19.4 -> 16.4 ms per batch)
-using CsrSmallK = CsrCfg<256, 16, 4, 2, GM_DEEP_PCT, GM_DRAIN>;
+using CsrSmallK = CsrCfg<256, GM_NB, GM_VSMALL, GM_MINB, GM_DEEP_PCT, GM_DRAIN, 12>;
 
 template <class C, class IdT, class WT>
 int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k,
@@ -769,8 +781,11 @@ static int csr_dispatch(const void* ids, int id_bits, const void* w, int w_bits,
 #define GM_CSR_LAUNCH(I, W)                                                                                          \
   rc = small_k ? launch_csr<CsrSmallK, I, W>(ids, w, offsets, n_vec, kk, useed, salt, vseeds, one_vec, y_out,     \
                                              s_out, emitted_out, ws, st, a0)                                         \
-               : launch_csr<CsrDefault, I, W>(ids, w, offsets, n_vec, kk, useed, salt, vseeds, one_vec, y_out,    \
-                                              s_out, emitted_out, ws, st, a0)
+       : kk <= CsrDefault::KMAX                                                                                      \
+           ? launch_csr<CsrDefault, I, W>(ids, w, offsets, n_vec, kk, useed, salt, vseeds, one_vec, y_out, s_out,   \
+                                          emitted_out, ws, st, a0)                                                   \
+           : launch_csr<CsrLargeK, I, W>(ids, w, offsets, n_vec, kk, useed, salt, vseeds, one_vec, y_out, s_out,    \
+                                         emitted_out, ws, st, a0)
   if (id_bits == 32 && w_bits == 32) GM_CSR_LAUNCH(u32, float);
   else if (id_bits == 32) GM_CSR_LAUNCH(u32, double);
   else if (w_bits == 32) GM_CSR_LAUNCH(u64, float);

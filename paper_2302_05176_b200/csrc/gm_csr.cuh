@@ -35,7 +35,7 @@ namespace gmk {
 #define GM_U 4
 #endif
 
-template <int NT_, int NB_, int V_ = 2, int MINB_ = 1, int DEEP_PCT_ = 62, int DRAIN_LIVE_ = 0>
+template <int NT_, int NB_, int V_ = 2, int MINB_ = 1, int DEEP_PCT_ = 62, int DRAIN_LIVE_ = 0, int PB_ = 16>
 struct CsrCfg {
   static constexpr int DRAIN_LIVE = DRAIN_LIVE_;  // queue empty and <= this many live lanes: warp-walk them
   static constexpr int NT = NT_;               // threads per CTA
@@ -48,10 +48,19 @@ struct CsrCfg {
   static constexpr int U = GM_U;               // lane steps per loop iteration
   static constexpr int MTAB = 256;             // Barrett table entries (z < MTAB)
   static constexpr int NMAX = (1 << 24) - 4096;  // elements per vector
+  // lane-table word: position and value - 1 in PB bits each; PB = 12 (k <=
+  // 4096) leaves the top 8 bits for the element's generation tag, so a lane
+  // starting an element retires the previous one's entries by bumping its
+  // tag instead of clearing the table (PB = 16: no tag, cleared per element)
+  static constexpr int PB = PB_;
+  static constexpr bool GEN = PB_ < 16;
+  static constexpr u32 VMASK = (1u << PB_) - 1u;
+  static constexpr u32 KMAX = 1u << PB_;       // largest k this configuration serves
   // expected depth at which an element goes straight to the warp walker
   static constexpr double kDeep = CAPI * (DEEP_PCT_ / 100.0);
   static_assert((NB_ & (NB_ - 1)) == 0, "NB must be a power of two");
   static_assert(V_ >= 1 && V_ <= 4, "1..4 slots");
+  static_assert(PB_ == 12 || PB_ == 16, "12-bit (tagged) or 16-bit lane-table words");
 };
 
 constexpr int SLOT_EMPTY = 0, SLOT_ACTIVE = 1;
@@ -63,9 +72,14 @@ struct SlotInfo {
   double tau;              // pass threshold
   double deep_w;           // weight at which an element is warp-walked
   unsigned long long emitted;
-  unsigned long long grab;  // (n << 32) | next element index: a ticket and the
-                            // element count it is valid for come from one atomic
   u64 useed, pseed;         // the vector's uniform / permutation stream seeds
+  // tickets: grab = (gen << 24) | next element index, hdr = (gen << 24) | n,
+  // gen counting the slot's passes.  hdr is published before grab, so a
+  // ticket is valid iff its gen matches hdr's and its index is below hdr's n
+  // (a ticket of an earlier pass can never validate against a later header)
+  unsigned grab;
+  unsigned hdr;
+  unsigned gen;
   int n;                   // elements
   int done;                // completed elements of this pass
   int attempt;
@@ -95,39 +109,54 @@ __device__ __forceinline__ uint4 tab_bucket(const u32* tab, u32 b) {
   return *reinterpret_cast<const uint4*>(tab + b * (C::NT * 4));
 }
 
-// Fast probe of one bucket for position p (p >= 1, or p = 0 whose identity
-// value 1 an empty word also yields): xor with p << 16 leaves the matching
-// word (at most one) below 2**16 with low half = value - 1.  Returns the min
-// over the 4 words (< 2**16 iff found).  Ways fill in order, so a bucket is
-// full iff its last word is non-zero and the first empty way is the number
-// of non-zero words among the first three.
-__device__ __forceinline__ u32 probe_min(const uint4 q, u32 p) {
-  const u32 k16 = p << 16;
-  return min(min(q.x ^ k16, q.y ^ k16), min(q.z ^ k16, q.w ^ k16));
-}
-__device__ __forceinline__ u32 first_empty(const uint4 q) { return q.z ? 3u : q.y ? 2u : q.x ? 1u : 0u; }
-
-// Full lookup (slow path): value at position p (identity if absent) | word
-// index of its entry << 16 (0x3FFF if absent) | first empty word on the
-// probe path << 30 (0x3FFF if none).
+// word of the current element: g24 = its generation << 24 (0 when PB = 16)
 template <class C>
-__device__ __noinline__ u64 tab_find(const u32* tab, u32 p) {
-  u32 val = p + 1, slot = 0x3FFFu, fre = 0x3FFFu, b = p & (C::NB - 1);
+__device__ __forceinline__ u32 tab_key(u32 p, u32 g24) { return g24 | (p << C::PB); }
+
+// a word belongs to the current element (PB = 16: any non-zero word)
+template <class C>
+__device__ __forceinline__ bool tab_live(u32 e, u32 g24) {
+  return C::GEN ? (e ^ g24) < (1u << 24) : e != 0u;
+}
+
+// Fast probe of one bucket for key tab_key(p) (p >= 1, or p = 0, whose
+// identity value 1 an empty PB = 16 word also yields): xor with the key
+// leaves the matching live word (at most one) below 2**PB with the low bits =
+// value - 1.  Returns the min over the 4 words (< 2**PB iff found).  Ways
+// fill in order within an element, so a bucket is full iff its last word is
+// live and the first free way is the number of live words among the first
+// three.
+__device__ __forceinline__ u32 probe_min(const uint4 q, u32 key) {
+  return min(min(q.x ^ key, q.y ^ key), min(q.z ^ key, q.w ^ key));
+}
+template <class C>
+__device__ __forceinline__ u32 first_empty(const uint4 q, u32 g24) {
+  return tab_live<C>(q.z, g24) ? 3u : tab_live<C>(q.y, g24) ? 2u : tab_live<C>(q.x, g24) ? 1u : 0u;
+}
+
+// Full lookup (slow path): value - 1 at position p (p if absent) | word
+// index of its entry << 16 (0x3FFF if absent) | first free word on the probe
+// path << 30 (0x3FFF if none).
+template <class C>
+__device__ __noinline__ u64 tab_find(const u32* tab, u32 p, u32 g24) {
+  const u32 key = tab_key<C>(p, g24);
+  u32 vm1 = p, slot = 0x3FFFu, fre = 0x3FFFu, b = p & (C::NB - 1);
   for (int it = 0; it < C::NB; ++it) {
     const uint4 q = tab_bucket<C>(tab, b);
     const u32 e[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
     for (int wy = 3; wy >= 0; --wy) {
-      if ((e[wy] >> 16) == p && e[wy] != 0u) {
+      const bool live = tab_live<C>(e[wy], g24);
+      if (live && (e[wy] ^ key) <= C::VMASK) {
         slot = b * 4 + wy;
-        val = (e[wy] & 0xFFFFu) + 1;
+        vm1 = e[wy] & C::VMASK;
       }
-      if (e[wy] == 0u) fre = b * 4 + wy;
+      if (!live) fre = b * 4 + wy;
     }
     if (slot != 0x3FFFu || fre != 0x3FFFu) break;
     b = (b + 1) & (C::NB - 1);
   }
-  return (u64)val | ((u64)slot << 16) | ((u64)fre << 30);
+  return (u64)vm1 | ((u64)slot << 16) | ((u64)fre << 30);
 }
 
 template <class C>
@@ -141,12 +170,29 @@ __device__ __forceinline__ void tab_clear(u32* tab) {
   for (int b = 0; b < C::NB; ++b) *reinterpret_cast<uint4*>(tab + b * (C::NT * 4)) = make_uint4(0, 0, 0, 0);
 }
 
+// the lane starts an element: retire the previous element's table entries
+// (bump the generation; clear the table when the tag wraps, or always when
+// PB = 16)
+template <class C>
+__device__ __forceinline__ void tab_next_element(u32* tab, u32& g24) {
+  if (C::GEN) {
+    g24 += 1u << 24;
+    if (g24 == 0u) {
+      tab_clear<C>(tab);
+      g24 = 1u << 24;
+    }
+  } else {
+    tab_clear<C>(tab);
+  }
+}
+
 // ---- lane walker state -----------------------------------------------------
 struct Lane {
   u64 id, ubase, pbase;
   double w, b, t, tau;
   Reg* regs;
   u32 z;
+  u32 g24;   // the element's lane-table generation << 24 (PB = 12)
   int used;
   int slot;
   bool fast;
@@ -161,25 +207,28 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
                                          const double* ltab) {
   const bool acc = !fresh;
   const u32 zs = L.z + 1;
+  const u32 g24 = L.g24;
   // permutation draw of step zs and both first-bucket probes
   const u64 g = mix64(L.pbase + (u64)zs * K_STEP);
   const u32 m = k - zs + 1;
   u32 ji = zs - 1 + mod_barrett64(g, m, mtab64[min(zs, (u32)C::MTAB - 1)]);
   const u32 zi = zs - 1;
   u32 bj = ji & (C::NB - 1);
+  const u32 kz = tab_key<C>(zi, g24);
+  u32 kj = tab_key<C>(ji, g24);
   uint4 qz = tab_bucket<C>(mytab, zi & (C::NB - 1)), qj = tab_bucket<C>(mytab, bj);
-  u32 mz = probe_min(qz, zi), mj = probe_min(qj, ji);
+  u32 mz = probe_min(qz, kz), mj = probe_min(qj, kj);
   // linear probing continues in the next bucket when the first is full:
   // look there too before falling back to the full lookup (branch-free: when
   // the first bucket settles it, the same bucket is simply read again)
   {
-    const u32 nz = ((mz >= 0x10000u) & (qz.w != 0u)) ? 1u : 0u;
-    const u32 nj = ((mj >= 0x10000u) & (qj.w != 0u)) ? 1u : 0u;
+    const u32 nz = ((mz > C::VMASK) & tab_live<C>(qz.w, g24)) ? 1u : 0u;
+    const u32 nj = ((mj > C::VMASK) & tab_live<C>(qj.w, g24)) ? 1u : 0u;
     bj = (bj + nj) & (C::NB - 1);
     qz = tab_bucket<C>(mytab, (zi + nz) & (C::NB - 1));
     qj = tab_bucket<C>(mytab, bj);
-    mz = probe_min(qz, zi);
-    mj = probe_min(qj, ji);
+    mz = probe_min(qz, kz);
+    mj = probe_min(qj, kj);
   }
   // next arrival's spacing (independent of this step's permutation work)
   const u32 zn = acc ? min(zs + 1, k) : 1u;
@@ -189,26 +238,26 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
   double dq = ddiv_fast(Lg, D);
   // fast case: no draw rejection, zi resolved in its first bucket, ji found
   // in its first bucket (overwrite) or absent with a free way there (insert)
-  const bool jfound = mj < 0x10000u;
+  const bool jfound = mj <= C::VMASK;
   const bool redraw = ((u32)(g >> 32) == 0xFFFFFFFFu) | (zs >= (u32)C::MTAB);  // the Barrett draw is not exact
-  const bool slow = acc & (redraw |
-                           ((mz >= 0x10000u) & (qz.w != 0u)) | (!jfound & (qj.w != 0u)));
-  u32 vz = mz < 0x10000u ? (mz & 0xFFFFu) + 1 : zi + 1;
-  u32 vj = jfound ? (mj & 0xFFFFu) + 1 : ji + 1;
-  const u32 k16 = ji << 16;
-  const u32 jway = jfound ? (((qj.x ^ k16) < 0x10000u) ? 0u : ((qj.y ^ k16) < 0x10000u) ? 1u
-                                                           : ((qj.z ^ k16) < 0x10000u) ? 2u : 3u)
-                          : first_empty(qj);
+  const bool slow = acc & (redraw | ((mz > C::VMASK) & tab_live<C>(qz.w, g24)) |
+                           (!jfound & tab_live<C>(qj.w, g24)));
+  u32 vz = mz <= C::VMASK ? mz + 1 : zi + 1;
+  u32 vj = jfound ? mj + 1 : ji + 1;
+  const u32 jway = jfound ? (((qj.x ^ kj) <= C::VMASK) ? 0u : ((qj.y ^ kj) <= C::VMASK) ? 1u
+                             : ((qj.z ^ kj) <= C::VMASK) ? 2u : 3u)
+                          : first_empty<C>(qj, g24);
   u32 put_slot = bj * 4 + jway;
   bool fresh_slot = !jfound;
-  if (!L.fast) dq = __ddiv_rn(Lg, D);
+  if (!L.fast) dq = ddiv_ieee(Lg, D);
   if (slow) {
     // a full first bucket alone keeps the fast draw; only a rejected draw or a
     // step beyond the Barrett table needs the exact one
     if (redraw) ji = perm_draw(L.pbase, zs, k) - 1;
-    vz = (u32)tab_find<C>(mytab, zi) & 0xFFFFu;
-    const u64 fj = tab_find<C>(mytab, ji);
-    vj = (u32)fj & 0xFFFFu;
+    kj = tab_key<C>(ji, g24);
+    vz = ((u32)tab_find<C>(mytab, zi, g24) & 0xFFFFu) + 1;
+    const u64 fj = tab_find<C>(mytab, ji, g24);
+    vj = ((u32)fj & 0xFFFFu) + 1;
     const u32 sj = (u32)(fj >> 16) & 0x3FFFu, fr = (u32)(fj >> 30) & 0x3FFFu;
     fresh_slot = sj == 0x3FFFu;
     put_slot = fresh_slot ? fr : sj;
@@ -219,35 +268,13 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
   if (acc & moved & !(!fresh_slot || (L.used < C::CAPI && put_slot != 0x3FFFu)))
     return 2;  // table full: hand over before step zs
   if (!moved) vj = vz;
-  if (acc & moved) tab_put<C>(mytab, put_slot, (ji << 16) | (vz - 1));
+  if (acc & moved) tab_put<C>(mytab, put_slot, kj | (vz - 1));
   L.used += (acc & moved & fresh_slot) ? 1 : 0;
   reg_min_lane(&L.regs[vj - 1], (u64)__double_as_longlong(L.t), L.id, acc);
   L.b = acc ? L.t : L.b;
   L.z = acc ? zs : L.z;
   L.t = __dadd_rn(L.b, dq);
   return (L.z >= k || L.t > L.tau) ? 1 : 0;
-}
-
-// One queue step zs (arrival time t) with full table lookups and the exact
-// draw: the slow path of the lane steps.  Returns false if the table is full
-// (nothing changed).
-template <class C>
-__device__ __noinline__ bool lane_step_generic(Lane& L, u32 zs, double t, u32* mytab, u32 k) {
-  const u32 ji = perm_draw(L.pbase, zs, k) - 1, zi = zs - 1;
-  const u32 vz = (u32)tab_find<C>(mytab, zi) & 0xFFFFu;
-  const u64 fj = tab_find<C>(mytab, ji);
-  u32 vj = (u32)fj & 0xFFFFu;
-  if (ji == zi) {
-    vj = vz;
-  } else {
-    const u32 sj = (u32)(fj >> 16) & 0x3FFFu, fr = (u32)(fj >> 30) & 0x3FFFu;
-    const bool fresh_slot = sj == 0x3FFFu;
-    if (fresh_slot && (L.used >= C::CAPI || fr == 0x3FFFu)) return false;
-    tab_put<C>(mytab, fresh_slot ? fr : sj, (ji << 16) | (vz - 1));
-    L.used += fresh_slot;
-  }
-  reg_min<true>(&L.regs[vj - 1], (u64)__double_as_longlong(t), L.id);
-  return true;
 }
 
 // ---- vector slots ----------------------------------------------------------
@@ -266,8 +293,17 @@ __device__ __forceinline__ void slot_open_pass(SlotInfo& sl, u32 k, int attempt,
   sl.deep_w = kdeep / ((double)k * sl.tau);
   sl.done = 0;
   sl.state = SLOT_ACTIVE;
+  const unsigned gen = (sl.gen + 1u) & 0xFFu;
+  sl.gen = gen;
+  *(volatile unsigned*)&sl.hdr = (gen << 24) | (unsigned)sl.n;
   __threadfence_block();
-  atomicExch(&sl.grab, (unsigned long long)(u32)sl.n << 32);
+  atomicExch(&sl.grab, gen << 24);
+}
+
+// a ticket t = atomicAdd(&grab, 1) is valid for the pass whose header h
+// (read after the atomic) has the same generation and more elements
+__device__ __forceinline__ bool ticket_valid(unsigned t, unsigned h) {
+  return ((t ^ h) >> 24) == 0u && (t & 0xFFFFFFu) < (h & 0xFFFFFFu);
 }
 
 // warp-uniform: take the next vector of the batch into slot s (or mark it
@@ -292,7 +328,11 @@ __device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const
     if (v >= n_vec) {
       if (lane == 0) {
         sl.state = SLOT_EMPTY;
-        atomicExch(&sl.grab, 0ull);
+        const unsigned gen = (sl.gen + 1u) & 0xFFu;
+        sl.gen = gen;
+        *(volatile unsigned*)&sl.hdr = gen << 24;  // n = 0: no ticket validates
+        __threadfence_block();
+        atomicExch(&sl.grab, gen << 24);
         __threadfence_block();
       }
       __syncwarp();

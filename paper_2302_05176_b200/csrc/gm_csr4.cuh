@@ -7,9 +7,11 @@
 // ticket on the oldest slot that still has untaken elements -- and keeps its
 // NEXT element taken and loading (id, weight from HBM/L2) while it walks the
 // current one, so a lane whose element ends goes on with the next one at the
-// next step, with no warp-wide hand-out and no idle steps.  A finished element
-// is counted lane by lane (its register updates fenced first); the lane that
-// counts a slot's last element flags it, and its warp finalises the slot:
+// next step, with no warp-wide hand-out and no idle steps.  A lane starting
+// an element retires its table by bumping a generation tag (k <= 4096), and
+// finished elements are counted per warp at the end of each round of lane
+// steps (one atomic per slot, the register updates fenced first); the warp
+// whose count completes a slot finalises it:
 // every register set -> write the sketch out and load the next vector; else
 // reopen the slot for the next pass with a larger tau.  Deep elements and
 // elements whose lane table fills up are walked by the whole warp (walk_warp).
@@ -65,6 +67,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     S.slot[tid].state = SLOT_EMPTY;
     S.slot[tid].n = 0;
     S.slot[tid].grab = 0;
+    S.slot[tid].hdr = 0;
+    S.slot[tid].gen = 0;
     S.slot[tid].seq = 0;
   }
   if (tid == 0) S.seq = 0;
@@ -82,6 +86,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   L.id = L.ubase = L.pbase = 0;
   L.regs = nullptr;
   L.fast = true;
+  L.g24 = C::GEN ? 1u << 24 : 0u;
   bool live = false, fresh = false, deep = false, resume = false;
   u32 em = 0;     // arrivals computed for the current element
   u32 fin = 0;    // slots this warp must finalise (warp-uniform)
@@ -102,7 +107,13 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   int nx_slot = 0;
   u64 nx_id = 0;
   double nx_w = 0.0;
-  u32 myfin = 0;  // slots whose last element this lane counted
+  // elements this lane finished in the current round, per slot (8 bits
+  // each), and their arrivals (counted mode); the warp adds them up per slot
+  // at the end of the round
+  u32 dpack = 0;
+  u32 emacc[V];
+#pragma unroll
+  for (int s = 0; s < V; ++s) emacc[s] = 0;
 
   // count `c` finished elements of slot s (lane 0; the warp's register
   // updates are fenced first).  n is read before the increment: once they are
@@ -128,20 +139,22 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     unsigned bseq = 0xFFFFFFFFu;
 #pragma unroll
     for (int s = 0; s < V; ++s) {
-      const unsigned long long g = *(volatile unsigned long long*)&S.slot[s].grab;
+      const unsigned g = *(volatile unsigned*)&S.slot[s].grab;
+      const unsigned h = *(volatile unsigned*)&S.slot[s].hdr;
       const unsigned q = *(volatile unsigned*)&S.slot[s].seq;
-      if ((u32)g < (u32)(g >> 32) && q < bseq) {
+      if (ticket_valid(g, h) && q < bseq) {
         bseq = q;
         best = s;
       }
     }
     if (best < 0) return;
-    const unsigned long long old = atomicAdd(&S.slot[best].grab, 1ull);
-    if ((u32)old >= (u32)(old >> 32)) return;  // the slot ran dry meanwhile
+    const unsigned t = atomicAdd(&S.slot[best].grab, 1u);
     __threadfence_block();
+    if (!ticket_valid(t, *(volatile unsigned*)&S.slot[best].hdr)) return;  // ran dry meanwhile
     const long long lo = *(volatile long long*)&S.slot[best].lo;
-    nx_id = (u64)__ldcg(&ids[lo + (u32)old]);  // L2-only loads: each element is read once
-    nx_w = (double)__ldcg(&wts[lo + (u32)old]);
+    const u32 i = t & 0xFFFFFFu;
+    nx_id = (u64)__ldcg(&ids[lo + i]);  // L2-only loads: each element is read once
+    nx_w = (double)__ldcg(&wts[lo + i]);
     nx_slot = best;
     nx_ok = true;
   };
@@ -164,19 +177,19 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     if (nx_w >= sl.deep_w) {
       deep = true;
     } else {
-      tab_clear<C>(mytab);
+      tab_next_element<C>(mytab, L.g24);
       live = true;
       fresh = true;
     }
   };
-  // lane-level: count the lane's finished element in its slot (its register
-  // updates fenced first); the lane that counts the last one flags the slot
+  // lane-level: note the lane's finished element (counted by the warp at the
+  // end of the round)
   auto finish_element = [&]() {
-    SlotInfo& sl = S.slot[L.slot];
-    const int n = *(volatile int*)&sl.n;
-    if (emitted_out) atomicAdd(&sl.emitted, (unsigned long long)em);
-    __threadfence_block();
-    if (atomicAdd(&sl.done, 1) + 1 == n) myfin |= 1u << L.slot;
+    dpack += 1u << (8 * L.slot);
+    if (emitted_out) {
+#pragma unroll
+      for (int s = 0; s < V; ++s) emacc[s] += L.slot == s ? em : 0u;
+    }
   };
 
 #ifdef GM_STATS
@@ -246,9 +259,11 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       }
       if (wres) {  // the source lane's live table entries -> dense array
         const u32* stab = tables + (warp * 32 + src) * 4;
+        const u32 sg24 = __shfl_sync(FULL, L.g24, src);
         for (u32 wi = lane; wi < (u32)C::SLOTS; wi += 32) {
           const u32 e = stab[(wi >> 2) * (NT * 4) + (wi & 3)];
-          if (e != 0u && (e >> 16) >= z0) dense[e >> 16] = (stamp << 16) | (e & 0xFFFFu);
+          const u32 pos = (e >> C::PB) & C::VMASK;
+          if (tab_live<C>(e, sg24) && pos >= z0) dense[pos] = (stamp << 16) | (e & C::VMASK);
         }
         __syncwarp();
       }
@@ -299,10 +314,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       bool work = false;
       if (lane == 0) {
 #pragma unroll
-        for (int s = 0; s < V; ++s) {
-          const unsigned long long g = *(volatile unsigned long long*)&S.slot[s].grab;
-          work |= (u32)g < (u32)(g >> 32);
-        }
+        for (int s = 0; s < V; ++s)
+          work |= ticket_valid(*(volatile unsigned*)&S.slot[s].grab, *(volatile unsigned*)&S.slot[s].hdr);
       }
       if (!__shfl_sync(FULL, (int)work, 0)) {
         if (live) {
@@ -335,8 +348,29 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         }
       }
     }
-    fin |= __reduce_or_sync(FULL, myfin);
-    myfin = 0;
+    // ---- (5) count the round's finished elements per slot (their register
+    // updates fenced first); the warp whose count completes a slot finalises it
+    if (u32 any = __reduce_or_sync(FULL, dpack)) {
+      __threadfence_block();
+#pragma unroll
+      for (int s = 0; s < V; ++s) {
+        if (!((any >> (8 * s)) & 0xFFu)) continue;  // no element of slot s finished
+        const u32 c = __reduce_add_sync(FULL, (dpack >> (8 * s)) & 0xFFu);
+        {
+          const u32 es = emitted_out ? __reduce_add_sync(FULL, emacc[s]) : 0u;
+          if (lane == 0) {
+            SlotInfo& sl = S.slot[s];
+            const int n = *(volatile int*)&sl.n;  // read before the count: the slot may then be reloaded
+            if (emitted_out) atomicAdd(&sl.emitted, (unsigned long long)es);
+            __threadfence_block();
+            if (atomicAdd(&sl.done, (int)c) + (int)c == n) fin |= 1u << s;
+          }
+          emacc[s] = 0;
+        }
+      }
+      fin = __shfl_sync(FULL, fin, 0);
+      dpack = 0;
+    }
   }
 }
 

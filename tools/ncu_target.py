@@ -3,7 +3,8 @@
   python tools/ncu_target.py --config N [--out gpurun_out/target_configN.json]
 
 Runs the roofline probe (chains 1, 2 and 4 -- the kernel arrival_probe_kernel)
-and two sketches of config N through the C ABI (configs 1-3: csr4_kernel;
+and sketches of config N through the C ABI (configs 1-3: csr4_kernel, two
+counted launches and a last one without counting, as bench.py runs it;
 4-5: the element-set kernels), and writes the per-launch work the evidence
 needs: algorithmic and executed arrivals per K1 launch, probe
 arrivals per launch.  tools/make_evidence.py joins it with the ncu CSV."""
@@ -57,6 +58,10 @@ def main():
             _device.call("gm_sketch_csr", d_ids.data_ptr(), 32, d_w.data_ptr(), 32, d_off.data_ptr(), n_vec, k,
                          sc.global_seed, sc.stream_salt, 0, y.data_ptr(), s.data_ptr(), em.data_ptr(), st.cuda_stream)
         info["executed_arrivals_per_launch"] = int(em.sum().item())
+        # the last launch (the one the evidence reads) runs as bench.py times
+        # it: no arrival counting
+        _device.call("gm_sketch_csr", d_ids.data_ptr(), 32, d_w.data_ptr(), 32, d_off.data_ptr(), n_vec, k,
+                     sc.global_seed, sc.stream_salt, 0, y.data_ptr(), s.data_ptr(), None, st.cuda_stream)
         info["algorithmic_arrivals_per_launch"] = bench.algorithmic_arrivals(dev, st, d_ids, 32, d_w, 32, d_off,
                                                                              n_vec, k, sc.global_seed, y)
         info["input_bytes"] = int(ids.nbytes + w.nbytes + off.nbytes)
@@ -66,6 +71,7 @@ def main():
         b = gm.sketch_vector_seeds(ids, w, k, [gm.SeedScheme(1 + r) for r in range(R)], counted=True)
         b = gm.sketch_vector_seeds(ids, w, k, [gm.SeedScheme(1 + r) for r in range(R)], counted=True)
         info["executed_arrivals_per_launch"] = int(b.emitted.sum().item())
+        b = gm.sketch_vector_seeds(ids, w, k, [gm.SeedScheme(1 + r) for r in range(R)])  # uncounted, last
     else:
         id_bits = ids.dtype.itemsize * 8
         d_ids = torch.from_numpy(ids.view(np.int64 if id_bits == 64 else np.int32)).to(dev)
