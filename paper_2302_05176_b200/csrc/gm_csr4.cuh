@@ -230,8 +230,14 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         GM_TRACE((unsigned long long)(v & 0xFFFFFFFF) | ((unsigned long long)att << 32) | (1ull << 40) |
                  ((unsigned long long)blockIdx.x << 48) | ((unsigned long long)s << 60));
       __syncwarp();
+#ifdef GM_STATS
+      const long long t_l0 = clock64();
+#endif
       slot_load<C, WT>(S, s, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list,
                        wts, useed, salt, vseeds, one_vec);
+#ifdef GM_STATS
+      if (lane == 0) atomicAdd(&g_stats[11], (unsigned long long)(clock64() - t_l0));
+#endif
     }
 
 #ifdef GM_STATS
@@ -298,6 +304,10 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 
     // ---- exit / idle
     if (!__any_sync(FULL, live || deep)) {
+      GM_STAT(0, lane == 0);  // idle iterations
+#ifdef GM_STATS
+    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 12; }
+#endif
       if (!__any_sync(FULL, nx_ok)) {
         bool open = false;
 #pragma unroll
@@ -328,10 +338,30 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       }
     }
 
+#ifdef GM_STATS
+    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 13; }
+#endif
     // ---- (4) u_run lane steps; a lane whose element ends counts it and goes on
     // with its prefetched element at the next step
 #pragma unroll 1
     for (int u = 0; u < u_run; ++u) {
+#ifdef GM_STATS
+      {
+        const unsigned lv = __ballot_sync(FULL, live), dp = __ballot_sync(FULL, deep);
+        const unsigned nn = __ballot_sync(FULL, !live && !deep);
+        bool avail = false;
+#pragma unroll
+        for (int s2 = 0; s2 < V; ++s2)
+          avail |= ticket_valid(*(volatile unsigned*)&S.slot[s2].grab, *(volatile unsigned*)&S.slot[s2].hdr);
+        if (lane == 0 && !avail) atomicAdd(&g_stats[7], (unsigned long long)__popc(nn));
+        if (lane == 0) {
+          atomicAdd(&g_stats[1], 1ull);
+          atomicAdd(&g_stats[2], (unsigned long long)__popc(lv));
+          atomicAdd(&g_stats[5], (unsigned long long)__popc(dp));
+          atomicAdd(&g_stats[6], (unsigned long long)__popc(nn));
+        }
+      }
+#endif
       if (live) {
         const int rc = lane_step<C>(L, fresh, mytab, mtab64, k, ltab);
         fresh = false;
@@ -348,6 +378,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         }
       }
     }
+#ifdef GM_STATS
+    { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 14; }
+#endif
     // ---- (5) count the round's finished elements per slot (their register
     // updates fenced first); the warp whose count completes a slot finalises it
     if (u32 any = __reduce_or_sync(FULL, dpack)) {

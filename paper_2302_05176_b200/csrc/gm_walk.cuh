@@ -125,12 +125,14 @@ __device__ __forceinline__ u32 dget(const D& dense, u32 pos, u32 stamp) {
 // permutation entries into `dense`.  scan: 32 doubles, prov: 32 ints (per-warp
 // shared scratch).  mtab: Barrett constants of m = k - z + 1 for z < mtab_n
 // (nullable).  unset_ctr: decremented when a register is first set (nullable).
+// ltab: the log table in shared memory (nullable: the global copy).
 template <bool kSharedRegs, bool kFast = false, class D>
 __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u64 useed,
                                           u64 pseed, const D& dense, u32 stamp, double* scan,
                                           int* prov, Reg* regs, int* unset_ctr, u32& emitted,
                                           u32 z_start = 0, double b_start = 0.0,
-                                          const u32* mtab = nullptr, u32 mtab_n = 0) {
+                                          const u32* mtab = nullptr, u32 mtab_n = 0,
+                                          const double* ltab = nullptr) {
   const unsigned FULL = 0xFFFFFFFFu;
   const int lane = threadIdx.x & 31;
   const u64 ubase = useed + id * K_ELEM;
@@ -140,7 +142,7 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
   while (z0 < k) {
     const u32 z = z0 + lane + 1;
     const bool valid = z <= k;
-    const double d = valid ? spacing_t<kFast>(ubase, z, w, k) : 0.0;
+    const double d = valid ? spacing_t<kFast>(ubase, z, w, k, ltab) : 0.0;
     scan[lane] = d;
     prov[lane] = -1;
     __syncwarp();

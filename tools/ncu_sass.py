@@ -1,6 +1,6 @@
 """List the SASS of an ncu source page (cuda,sass csv) in address order with
-warp instructions executed, active threads per instruction and the CUDA
-source line each belongs to.
+warp instructions executed, active threads per instruction, stall samples
+and the CUDA source line each belongs to.
 
   python tools/ncu_sass.py src.csv [min_count] > sass.txt
 """
@@ -39,12 +39,13 @@ def main(path, min_count=0):
                 return 0.0
         ie = f("Instructions Executed")
         te = f("Thread Instructions Executed")
-        out.append((addr, ie, te / ie if ie else 0.0, f"{cur_file}:{cur_line}", r[3].strip()))
+        out.append((addr, ie, te / ie if ie else 0.0, f"{cur_file}:{cur_line}", r[3].strip(),
+                    f("Warp Stall Sampling (All Samples)")))
     out.sort()
     base = out[0][0] if out else 0
-    for a, ie, thr, src, sass in out:
+    for a, ie, thr, src, sass, st in out:
         if ie >= float(min_count):
-            print(f"{a - base:06x} {ie:10.0f} {thr:5.1f} {src:26s} {sass}")
+            print(f"{a - base:06x} {ie:10.0f} {thr:5.1f} {st:7.0f} {src:26s} {sass}")
 
 
 if __name__ == "__main__":
