@@ -139,9 +139,19 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
   const u64 pbase = pseed + id * K_ELEM;
   double b = b_start;
   u32 z0 = z_start;
+  typedef std::remove_cv_t<std::remove_reference_t<decltype(dense[0])>> DW;
   while (z0 < k) {
     const u32 z = z0 + lane + 1;
     const bool valid = z <= k;
+    // the permutation draws and the dense-array reads first (they do not
+    // depend on the arrival times): the reads, L1/L2 round trips, then
+    // complete under the spacings and the prefix instead of after them
+    u32 j = 0;
+    if (valid) j = FyWord<DW>::BIG ? perm_draw_big(pbase, z, k)
+                   : (mtab && z < mtab_n) ? perm_draw_m(pbase, z, k, mtab[z]) : perm_draw(pbase, z, k);
+    const u32 zi = z - 1, ji = j - 1;
+    u32 vz = valid ? dget(dense, zi, stamp) : 0u;
+    const u32 mj = valid ? dget(dense, ji, stamp) : 0u;
     const double d = valid ? spacing_t<kFast>(ubase, z, w, k, ltab) : 0.0;
     scan[lane] = d;
     prov[lane] = -1;
@@ -167,13 +177,6 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
     const u32 stop = __ballot_sync(FULL, !(valid && t <= tau));
     const int n_acc = stop ? __ffs(stop) - 1 : 32;
     const bool acc = lane < n_acc;
-    u32 j = 0;
-    typedef std::remove_cv_t<std::remove_reference_t<decltype(dense[0])>> DW;
-    if (acc) j = FyWord<DW>::BIG ? perm_draw_big(pbase, z, k)
-                 : (mtab && z < mtab_n) ? perm_draw_m(pbase, z, k, mtab[z]) : perm_draw(pbase, z, k);
-    const u32 zi = z - 1, ji = j - 1;
-    u32 vz = acc ? dget(dense, zi, stamp) : 0u;
-    const u32 mj = acc ? dget(dense, ji, stamp) : 0u;
     // provider of position zi: last earlier lane whose ji == zi
     const int tgt = (int)ji - (int)z0;
     if (acc && tgt > lane && tgt < n_acc) atomicMax(&prov[tgt], lane);
