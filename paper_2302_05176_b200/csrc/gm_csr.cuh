@@ -59,7 +59,9 @@ struct CsrCfg {
   // expected depth at which an element goes straight to the warp walker
   static constexpr double kDeep = CAPI * (DEEP_PCT_ / 100.0);
   static_assert((NB_ & (NB_ - 1)) == 0, "NB must be a power of two");
-  static_assert(V_ >= 1 && V_ <= 4, "1..4 slots");
+  static_assert(V_ >= 1 && V_ <= 8, "1..8 slots");
+  // per-slot field width of a lane's packed finished-element counts
+  static constexpr int FW = V_ <= 4 ? 8 : V_ <= 5 ? 6 : 4;
   static_assert(PB_ == 12 || PB_ == 16, "12-bit (tagged) or 16-bit lane-table words");
 };
 
@@ -89,7 +91,7 @@ struct SlotInfo {
 };
 
 struct CsrShared {
-  SlotInfo slot[4];
+  SlotInfo slot[8];
   unsigned seq;
 };
 

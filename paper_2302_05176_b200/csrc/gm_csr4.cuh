@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   int nx_slot = 0;
   u64 nx_id = 0;
   double nx_w = 0.0;
-  // elements this lane finished in the current round, per slot (8 bits
-  // each), and their arrivals (counted mode); the warp adds them up per slot
+  // elements this lane finished in the current round, per slot (C::FW bits
+  // each: at most u_run + 1 per round), and their arrivals (counted mode); the warp adds them up per slot
   // at the end of the round
   u32 dpack = 0;
   u32 emacc[V];
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   // lane-level: note the lane's finished element (counted by the warp at the
   // end of the round)
   auto finish_element = [&]() {
-    dpack += 1u << (8 * L.slot);
+    dpack += 1u << (C::FW * L.slot);
     if (emitted_out) {
 #pragma unroll
       for (int s = 0; s < V; ++s) emacc[s] += L.slot == s ? em : 0u;
@@ -387,8 +387,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       __threadfence_block();
 #pragma unroll
       for (int s = 0; s < V; ++s) {
-        if (!((any >> (8 * s)) & 0xFFu)) continue;  // no element of slot s finished
-        const u32 c = __reduce_add_sync(FULL, (dpack >> (8 * s)) & 0xFFu);
+        constexpr u32 FM = (1u << C::FW) - 1u;
+        if (!((any >> (C::FW * s)) & FM)) continue;  // no element of slot s finished
+        const u32 c = __reduce_add_sync(FULL, (dpack >> (C::FW * s)) & FM);
         {
           const u32 es = emitted_out ? __reduce_add_sync(FULL, emacc[s]) : 0u;
           if (lane == 0) {
