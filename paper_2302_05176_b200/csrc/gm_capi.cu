@@ -203,7 +203,7 @@ using CsrLargeK = CsrCfg<256, 16, 2, 2, GM_DEEP_PCT, GM_DRAIN, 16>;
 // take, so a CTA keeps four (small) vectors in flight -- fewer lanes idle
 // while a slot drains (config 3: 19.4 -> 16.4 ms per batch)
 using CsrSmallK = CsrCfg<GM_NT, GM_NB, GM_VSMALL, GM_MINB, GM_DEEP_PCT, GM_DRAIN, 12>;
-// One vector under many seeds (GM_FLAG_ONE_VECTOR, k <= 1024): every slot
+// One vector under many seeds (GM_FLAG_ONE_VECTOR, k <= 512): every slot
 // holds the same vector, so a slot's elements outnumber the lanes and two
 // slots keep a 512-thread CTA busy; with few slots, element turnover (the
 // ticket scan over the slots) is cheapest (config 1: 0.585 ms with the
@@ -212,7 +212,13 @@ using CsrSmallK = CsrCfg<GM_NT, GM_NB, GM_VSMALL, GM_MINB, GM_DEEP_PCT, GM_DRAIN
 #ifndef GM_VONE
 #define GM_VONE 2
 #endif
-using CsrOneVec = CsrCfg<512, GM_NB, GM_VONE, 1, GM_DEEP_PCT, GM_DRAIN, 12>;
+#ifndef GM_WQ_ONE
+#define GM_WQ_ONE 128
+#endif
+#ifndef GM_QCAP_ONE
+#define GM_QCAP_ONE 64
+#endif
+using CsrOneVec = CsrCfg<512, GM_NB, GM_VONE, 1, GM_DEEP_PCT, GM_DRAIN, 12, GM_WQ_ONE, GM_QCAP_ONE>;
 
 template <class C, class IdT, class WT>
 int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k,
@@ -795,7 +801,7 @@ static int csr_dispatch(const void* ids, int id_bits, const void* w, int w_bits,
   // exhaustive = a single pass with tau = +inf (pass_tau's last attempt)
   const int a0 = (flags & GM_FLAG_EXHAUSTIVE) ? 3 : 0;
 #define GM_CSR_LAUNCH(I, W)                                                                                          \
-  rc = one_vec && kk <= 1024                                                                                   \
+  rc = one_vec && kk <= 512                                                                                    \
            ? launch_csr<CsrOneVec, I, W>(ids, w, offsets, n_vec, kk, useed, salt, vseeds, one_vec, y_out, s_out,   \
                                          emitted_out, ws, st, a0)                                                    \
        : small_k ? launch_csr<CsrSmallK, I, W>(ids, w, offsets, n_vec, kk, useed, salt, vseeds, one_vec, y_out,     \

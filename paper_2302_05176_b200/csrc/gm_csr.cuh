@@ -35,8 +35,19 @@ namespace gmk {
 #define GM_U 4
 #endif
 
-template <int NT_, int NB_, int V_ = 2, int MINB_ = 1, int DEEP_PCT_ = 62, int DRAIN_LIVE_ = 0, int PB_ = 16>
+template <int NT_, int NB_, int V_ = 2, int MINB_ = 1, int DEEP_PCT_ = 62, int DRAIN_LIVE_ = 0, int PB_ = 16,
+          int WQ_ = 0, int QCAP_ = 64>
 struct CsrCfg {
+  // WQ > 0: elements reach the lanes through a per-warp queue instead of
+  // per-lane tickets: the warp takes WQ tickets at a time, stages their ids
+  // and weights in shared memory (cp.async, in flight during a round of lane
+  // steps), tests every element's first arrival against the pass's tau with
+  // the K2 filter's exact-safe fp32 bound, counts the ones that cannot reach
+  // tau as finished (one arrival each) and queues the rest for the lanes
+  static constexpr int WQ = WQ_;
+  static constexpr int QCAP = WQ_ > 0 ? QCAP_ : 1;  // queued survivors per warp (ring; the test of a
+                                                     // staged batch pauses while the ring is full)
+  static_assert(WQ_ == 0 || (QCAP_ >= 32 && WQ_ % 32 == 0), "WQ: whole warps of tickets, ring >= 32");
   static constexpr int DRAIN_LIVE = DRAIN_LIVE_;  // queue empty and <= this many live lanes: warp-walk them
   static constexpr int NT = NT_;               // threads per CTA
   static constexpr int NWARP = NT_ / 32;
@@ -93,6 +104,10 @@ struct SlotInfo {
 struct CsrShared {
   SlotInfo slot[8];
   unsigned seq;
+  // one vector under many seeds: its weight sum, divide range and validity
+  // are the same for every sketch -- computed by the first slot load, reused
+  double one_W;
+  int one_fast, one_state;  // one_state: 0 unknown, 1 valid, 2 invalid weights
 };
 
 template <class C>
@@ -102,7 +117,9 @@ __host__ __device__ constexpr size_t csr_smem_bytes(u32 k) {
          + (size_t)C::MTAB * 4                       // Barrett table
          + 128 * 16                                  // log table copy
          + (size_t)C::NWARP * 32 * (8 + 4)           // warp-walker scan + prov
-         + (size_t)C::MTAB * 8;                      // 64-bit Barrett table
+         + (size_t)C::MTAB * 8                       // 64-bit Barrett table
+         + (C::WQ > 0 ? (size_t)C::NWARP * (8 + C::WQ * 16 + C::QCAP * 20) : 0);  // WQ: ring positions,
+                                                                                // staging, ring
 }
 
 // ---- lane table ----------------------------------------------------------
@@ -317,7 +334,7 @@ __device__ __forceinline__ bool ticket_valid(unsigned t, unsigned h) {
 // for this vector, in the same order: the same W), so the batch needs no
 // prep launch.
 template <class C, class WT>
-__device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const int64_t* offsets,
+__device__ __noinline__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const int64_t* offsets,
                           int64_t n_vec, const double* Wsum, const int* vflags, int* vec_counter,
                           unsigned long long* err, int attempt0, int lane, const int* vec_list,
                           const WT* wts, u64 useed, u64 salt, const u64* vseeds, int one_vec) {
@@ -355,7 +372,15 @@ __device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const
     }
     double W = 0.0;
     int fast = 1;
-    if (!Wsum) {
+    const int ostate = one_vec ? *(volatile int*)&S.one_state : 0;
+    if (ostate == 1) {  // the one vector's sum, computed by an earlier slot load
+      __threadfence_block();
+      W = *(volatile double*)&S.one_W;
+      fast = *(volatile int*)&S.one_fast;
+    } else if (ostate == 2) {
+      if (lane == 0) atomicCAS(err, 0ull, ((unsigned long long)(v & 0xFFFFFFFF) << 32) | 2u);
+      continue;
+    } else if (!Wsum) {
       int bad = 0;
       for (int64_t i0 = lo + lane; i0 < lo + n; i0 += 8 * 32) {  // 8 loads in flight per lane
         WT wv[8];
@@ -374,7 +399,14 @@ __device__ void slot_load(CsrShared& S, int s, unsigned char* smem, u32 k, const
 #pragma unroll
       for (int o = 16; o; o >>= 1) W += __shfl_xor_sync(FULL, W, o);
       fast = __all_sync(FULL, fast);
-      if (__any_sync(FULL, bad)) {
+      const bool any_bad = __any_sync(FULL, bad);
+      if (one_vec && lane == 0) {  // (two first loads may both get here: same values)
+        S.one_W = W;
+        S.one_fast = fast;
+        __threadfence_block();
+        *(volatile int*)&S.one_state = any_bad ? 2 : 1;
+      }
+      if (any_bad) {
         if (lane == 0) atomicCAS(err, 0ull, ((unsigned long long)(v & 0xFFFFFFFF) << 32) | 2u);
         continue;
       }

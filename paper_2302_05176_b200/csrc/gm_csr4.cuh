@@ -54,6 +54,15 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   // floor(2^64 / m) for m = k - z + 1, z < MTAB: the lane step's draw in one 64-bit Barrett reduction
   u64* mtab64 = reinterpret_cast<u64*>(reinterpret_cast<int*>(ltab + 256 + NWARP * 32) + NWARP * 32);
   u32* mytab = tables + tid * 4;
+  // WQ: this warp's staging area (ids, weights of a ticket batch) and queue
+  unsigned char* wq_area = reinterpret_cast<unsigned char*>(mtab64 + C::MTAB) + (size_t)warp * (8 + C::WQ * 16 + C::QCAP * 20);
+  int* q_pos = reinterpret_cast<int*>(wq_area);  // [0] head, [1] tail: monotone ring positions
+  unsigned char* wq_base = wq_area + 8;
+  IdT* st_id = reinterpret_cast<IdT*>(wq_base);
+  WT* st_w = reinterpret_cast<WT*>(wq_base + C::WQ * 8);
+  u64* q_id = reinterpret_cast<u64*>(wq_base + C::WQ * 16);
+  double* q_w = reinterpret_cast<double*>(wq_base + C::WQ * 16 + C::QCAP * 8);
+  int* q_slot = reinterpret_cast<int*>(wq_base + C::WQ * 16 + C::QCAP * 16);
   u32* dense = dense_global + ((size_t)blockIdx.x * NWARP + warp) * k;
 
   for (u32 z = tid; z < (u32)C::MTAB; z += NT) {
@@ -62,6 +71,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   }
   for (u32 i = tid; i < 256; i += NT) ltab[i] = gm_glog_tab[i >> 1][i & 1];
   tab_clear<C>(mytab);
+  if (C::WQ > 0 && lane == 0) q_pos[0] = q_pos[1] = 0;
   for (u32 i = lane; i < k; i += 32) dense[i] = 0;  // stamps restart every launch
   if (tid < V) {
     S.slot[tid].state = SLOT_EMPTY;
@@ -71,7 +81,10 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     S.slot[tid].gen = 0;
     S.slot[tid].seq = 0;
   }
-  if (tid == 0) S.seq = 0;
+  if (tid == 0) {
+    S.seq = 0;
+    S.one_state = 0;
+  }
   __syncthreads();
   if (warp < V)
     slot_load<C, WT>(S, warp, smem_raw, k, offsets, n_vec, Wsum, vflags, vec_counter, err, attempt0, lane, vec_list,
@@ -107,6 +120,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   int nx_slot = 0;
   u64 nx_id = 0;
   double nx_w = 0.0;
+  // WQ: the warp's ticket batch in flight (warp-uniform): slot, element count
+  int b_slot = -1;
+  u32 b_cnt = 0, b_pos = 0;  // staged elements, elements tested so far
   // elements this lane finished in the current round, per slot (C::FW bits
   // each: at most u_run + 1 per round), and their arrivals (counted mode); the warp adds them up per slot
   // at the end of the round
@@ -135,6 +151,16 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   // lane-level: take a ticket from the oldest slot with untaken elements and
   // start loading that element (its id and weight are read at start_next)
   auto take_next = [&]() {
+    if constexpr (C::WQ > 0) {  // pop a tested survivor from the warp's queue
+      const int h = atomicAdd(&q_pos[0], 1);
+      if (h >= *(volatile int*)&q_pos[1]) return;  // empty (the refill clamps qhead back)
+      const int e = h % C::QCAP;
+      nx_id = q_id[e];
+      nx_w = q_w[e];
+      nx_slot = q_slot[e];
+      nx_ok = true;
+      return;
+    }
     int best = -1;
     unsigned bseq = 0xFFFFFFFFu;
 #pragma unroll
@@ -190,6 +216,133 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 #pragma unroll
       for (int s = 0; s < V; ++s) emacc[s] += L.slot == s ? em : 0u;
     }
+  };
+
+  // count the finished elements per slot (their register updates fenced
+  // first); the warp whose count completes a slot finalises it.  Every path
+  // through the loop ends with it, so no count stays pending while a warp idles.
+  auto flush_counts = [&]() {
+    if (u32 any = __reduce_or_sync(FULL, dpack)) {
+      __threadfence_block();
+#pragma unroll
+      for (int s = 0; s < V; ++s) {
+        constexpr u32 FM = (1u << C::FW) - 1u;
+        if (!((any >> (C::FW * s)) & FM)) continue;  // no element of slot s finished
+        const u32 c = __reduce_add_sync(FULL, (dpack >> (C::FW * s)) & FM);
+        {
+          const u32 es = emitted_out ? __reduce_add_sync(FULL, emacc[s]) : 0u;
+          if (lane == 0) {
+            SlotInfo& sl = S.slot[s];
+            const int n = *(volatile int*)&sl.n;  // read before the count: the slot may then be reloaded
+            if (emitted_out) atomicAdd(&sl.emitted, (unsigned long long)es);
+            __threadfence_block();
+            if (atomicAdd(&sl.done, (int)c) + (int)c == n) fin |= 1u << s;
+          }
+          emacc[s] = 0;
+        }
+      }
+      fin = __shfl_sync(FULL, fin, 0);
+      dpack = 0;
+    }
+  };
+
+  // WQ (warp-uniform): test the staged batch -- survivors to the queue,
+  // elements whose first arrival cannot reach tau counted as finished -- then
+  // take the next batch of tickets and start its copies into the staging area
+  auto refill = [&]() {
+    if (b_slot >= 0) {
+      if (b_pos == 0) {
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncwarp();
+      }
+      SlotInfo& sl = S.slot[b_slot];
+      const double tk = *(volatile double*)&sl.tau * (double)k;
+      const float tkf = (float)tk;
+      const u64 c0 = *(volatile u64*)&sl.useed + K_STEP;
+      const int t0 = *(volatile int*)&q_pos[1];
+      const int head = min(*(volatile int*)&q_pos[0], t0);  // pops may have run past the tail
+      int tail = t0;
+      u32 skips = 0;
+      for (; b_pos < b_cnt && tail - head + 32 <= C::QCAP; b_pos += 32) {
+        const u32 i = b_pos + lane;
+        const bool valid = i < b_cnt;
+        const u64 id = valid ? (u64)st_id[i] : 0ull;
+        const WT wv = valid ? st_w[i] : WT(0);
+        const bool sk = valid && filter_skip_f(c0 + id * K_ELEM, filter_x(wv, tkf, tk));
+        const bool kp = valid && !sk;
+        const unsigned m = __ballot_sync(FULL, kp);
+        if (kp) {
+          const int e = (tail + __popc(m & lt_mask)) % C::QCAP;
+          q_id[e] = id;
+          q_w[e] = (double)wv;
+          q_slot[e] = b_slot;
+        }
+        tail += __popc(m);
+        skips += sk ? 1u : 0u;
+      }
+      dpack += skips << (C::FW * b_slot);
+      if (emitted_out) {
+#pragma unroll
+        for (int s2 = 0; s2 < V; ++s2) emacc[s2] += b_slot == s2 ? skips : 0u;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        q_pos[0] = head;
+        __threadfence_block();
+        *(volatile int*)&q_pos[1] = tail;
+      }
+      __syncwarp();
+      if (b_pos < b_cnt) return;  // ring full: the rest of the batch waits
+      b_slot = -1;
+    }
+    // the next batch of tickets
+    int best = -1;
+    u32 base = 0, cnt = 0;
+    if (lane == 0) {
+      unsigned bseq = 0xFFFFFFFFu;
+#pragma unroll
+      for (int s2 = 0; s2 < V; ++s2) {
+        const unsigned g = *(volatile unsigned*)&S.slot[s2].grab;
+        const unsigned h = *(volatile unsigned*)&S.slot[s2].hdr;
+        const unsigned q = *(volatile unsigned*)&S.slot[s2].seq;
+        if (ticket_valid(g, h) && q < bseq) {
+          bseq = q;
+          best = s2;
+        }
+      }
+      if (best >= 0) {
+        const unsigned t = atomicAdd(&S.slot[best].grab, (unsigned)C::WQ);
+        __threadfence_block();
+        const unsigned h = *(volatile unsigned*)&S.slot[best].hdr;
+        if (ticket_valid(t, h)) {
+          base = t & 0xFFFFFFu;
+          cnt = min((u32)C::WQ, (h & 0xFFFFFFu) - base);
+        } else {
+          best = -1;
+        }
+      }
+    }
+    best = __shfl_sync(FULL, best, 0);
+    if (best < 0) return;
+    base = __shfl_sync(FULL, base, 0);
+    cnt = __shfl_sync(FULL, cnt, 0);
+    const long long lo = *(volatile long long*)&S.slot[best].lo;
+    for (u32 i = lane; i < cnt; i += 32) {
+      const u32 ds = (u32)__cvta_generic_to_shared(&st_id[i]);
+      const u32 dw = (u32)__cvta_generic_to_shared(&st_w[i]);
+      if (sizeof(IdT) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(ds), "l"(&ids[lo + base + i]) : "memory");
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(ds), "l"(&ids[lo + base + i]) : "memory");
+      if (sizeof(WT) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dw), "l"(&wts[lo + base + i]) : "memory");
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dw), "l"(&wts[lo + base + i]) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    b_slot = best;
+    b_cnt = cnt;
+    b_pos = 0;
   };
 
 #ifdef GM_STATS
@@ -275,12 +428,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       }
       u32 wem = 0;
       Reg* regs = slot_regs<C>(smem_raw, s, k);
-      if (wfast)
-        walk_warp<true, true>(wid, ww, tau, k, wus, wps, dense, stamp, scan, prov, regs, nullptr, wem, z0, b0,
-                              mtab, (u32)C::MTAB);
-      else
-        walk_warp<true, false>(wid, ww, tau, k, wus, wps, dense, stamp, scan, prov, regs, nullptr, wem, z0, b0,
-                               mtab, (u32)C::MTAB);
+      walk_warp<true>(wid, ww, tau, k, wus, wps, dense, stamp, scan, prov, regs, nullptr, wem, z0, b0, mtab,
+                      (u32)C::MTAB, nullptr, wfast);
       wem = __shfl_sync(FULL, wem, 0);
       GM_STAT(3, lane == 0);  // warp walks
       GM_STAT(4, lane == 0 ? wem : 0u);
@@ -296,6 +445,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 #endif
     // ---- (3) lanes without an element start the one they prefetched (or take
     // one now), and every lane keeps its next element in flight
+    if constexpr (C::WQ > 0) refill();
     if (!live && !deep) {
       if (!nx_ok) take_next();
       if (nx_ok) start_next();
@@ -304,11 +454,19 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 
     // ---- exit / idle
     if (!__any_sync(FULL, live || deep)) {
+#ifndef GM_IDLE_FLUSH_ALL
+      if constexpr (C::WQ > 0) flush_counts();  // (skips counted by a refill)
+#else
+      flush_counts();
+#endif
       GM_STAT(0, lane == 0);  // idle iterations
 #ifdef GM_STATS
     { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 12; }
 #endif
-      if (!__any_sync(FULL, nx_ok)) {
+      bool queued = false;
+      if constexpr (C::WQ > 0)
+        queued = b_slot >= 0 || *(volatile int*)&q_pos[1] > *(volatile int*)&q_pos[0];
+      if (!__any_sync(FULL, nx_ok) && !queued) {
         bool open = false;
 #pragma unroll
         for (int s = 0; s < V; ++s) open |= *(volatile int*)&S.slot[s].state != SLOT_EMPTY;
@@ -322,6 +480,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     // hand their elements to the warp walker (all 32 lanes on each)
     if (C::DRAIN_LIVE > 0 && !__any_sync(FULL, nx_ok) && __popc(__ballot_sync(FULL, live)) <= C::DRAIN_LIVE) {
       bool work = false;
+      if constexpr (C::WQ > 0)
+        work = b_slot >= 0 || *(volatile int*)&q_pos[1] > *(volatile int*)&q_pos[0];
       if (lane == 0) {
 #pragma unroll
         for (int s = 0; s < V; ++s)
@@ -334,6 +494,11 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
           deep = true;
           resume = true;
         }
+#ifndef GM_IDLE_FLUSH_ALL
+        if constexpr (C::WQ > 0) flush_counts();
+#else
+        flush_counts();
+#endif
         continue;
       }
     }
@@ -381,30 +546,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 #ifdef GM_STATS
     { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 14; }
 #endif
-    // ---- (5) count the round's finished elements per slot (their register
-    // updates fenced first); the warp whose count completes a slot finalises it
-    if (u32 any = __reduce_or_sync(FULL, dpack)) {
-      __threadfence_block();
-#pragma unroll
-      for (int s = 0; s < V; ++s) {
-        constexpr u32 FM = (1u << C::FW) - 1u;
-        if (!((any >> (C::FW * s)) & FM)) continue;  // no element of slot s finished
-        const u32 c = __reduce_add_sync(FULL, (dpack >> (C::FW * s)) & FM);
-        {
-          const u32 es = emitted_out ? __reduce_add_sync(FULL, emacc[s]) : 0u;
-          if (lane == 0) {
-            SlotInfo& sl = S.slot[s];
-            const int n = *(volatile int*)&sl.n;  // read before the count: the slot may then be reloaded
-            if (emitted_out) atomicAdd(&sl.emitted, (unsigned long long)es);
-            __threadfence_block();
-            if (atomicAdd(&sl.done, (int)c) + (int)c == n) fin |= 1u << s;
-          }
-          emacc[s] = 0;
-        }
-      }
-      fin = __shfl_sync(FULL, fin, 0);
-      dpack = 0;
-    }
+    // ---- (5) count the round's finished elements
+    flush_counts();
   }
 }
 

@@ -126,13 +126,17 @@ __device__ __forceinline__ u32 dget(const D& dense, u32 pos, u32 stamp) {
 // shared scratch).  mtab: Barrett constants of m = k - z + 1 for z < mtab_n
 // (nullable).  unset_ctr: decremented when a register is first set (nullable).
 // ltab: the log table in shared memory (nullable: the global copy).
-template <bool kSharedRegs, bool kFast = false, class D>
+// fast: every spacing divide of the element may use the branch-free divide
+// (w_fast(w)); a run-time flag, so one copy of the walker serves both
+// (kernel code size: the K1 kernel keeps its hot loops in the instruction
+// cache).
+template <bool kSharedRegs, class D>
 __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u64 useed,
                                           u64 pseed, const D& dense, u32 stamp, double* scan,
                                           int* prov, Reg* regs, int* unset_ctr, u32& emitted,
                                           u32 z_start = 0, double b_start = 0.0,
                                           const u32* mtab = nullptr, u32 mtab_n = 0,
-                                          const double* ltab = nullptr) {
+                                          const double* ltab = nullptr, bool fast = false) {
   const unsigned FULL = 0xFFFFFFFFu;
   const int lane = threadIdx.x & 31;
   const u64 ubase = useed + id * K_ELEM;
@@ -152,7 +156,13 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
     const u32 zi = z - 1, ji = j - 1;
     u32 vz = valid ? dget(dense, zi, stamp) : 0u;
     const u32 mj = valid ? dget(dense, ji, stamp) : 0u;
-    const double d = valid ? spacing_t<kFast>(ubase, z, w, k, ltab) : 0.0;
+    double d = 0.0;
+    if (valid) {
+      const u64 x = mix64(ubase + (u64)z * K_STEP);
+      const double L = ltab ? -log_pos_t(u_open(x), ltab) : -log_pos(u_open(x));
+      const double D = __dmul_rn(w, (double)(k - z + 1));
+      d = fast ? ddiv_fast(L, D) : ddiv_ieee(L, D);
+    }
     scan[lane] = d;
     prov[lane] = -1;
     __syncwarp();
