@@ -27,6 +27,17 @@
 
 namespace gmk {
 
+#ifdef GM_WALK_NOINLINE
+// the warp walker as a call (kernel code size)
+template <class D>
+__device__ __noinline__ void csr_walk(u64 id, double w, double tau, u32 k, u64 useed, u64 pseed, const D dense,
+                                      u32 stamp, double* scan, int* prov, Reg* regs, u32& emitted, u32 z0,
+                                      double b0, const u32* mtab, u32 mtab_n, bool fast) {
+  walk_warp<true>(id, w, tau, k, useed, pseed, dense, stamp, scan, prov, regs, nullptr, emitted, z0, b0, mtab,
+                  mtab_n, nullptr, fast);
+}
+#endif
+
 // Dynamic shared memory: Reg regs[V][k] | u32 tables[NB][NT][4] | u32 mtab[MTAB]
 //   | double scan[NWARP][32] | int prov[NWARP][32]
 template <class C, class IdT, class WT>
@@ -224,21 +235,29 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   auto flush_counts = [&]() {
     if (u32 any = __reduce_or_sync(FULL, dpack)) {
       __threadfence_block();
-#pragma unroll
-      for (int s = 0; s < V; ++s) {
-        constexpr u32 FM = (1u << C::FW) - 1u;
-        if (!((any >> (C::FW * s)) & FM)) continue;  // no element of slot s finished
+      constexpr u32 FM = (1u << C::FW) - 1u;
+      // over the slots with finished elements only (one copy of the body:
+      // kernel code size)
+      for (u32 live_s = 0, am = any; am; am >>= C::FW, ++live_s) {
+        if (!(am & FM)) continue;  // no element of slot live_s finished
+        const int s = (int)live_s;
         const u32 c = __reduce_add_sync(FULL, (dpack >> (C::FW * s)) & FM);
-        {
-          const u32 es = emitted_out ? __reduce_add_sync(FULL, emacc[s]) : 0u;
-          if (lane == 0) {
-            SlotInfo& sl = S.slot[s];
-            const int n = *(volatile int*)&sl.n;  // read before the count: the slot may then be reloaded
-            if (emitted_out) atomicAdd(&sl.emitted, (unsigned long long)es);
-            __threadfence_block();
-            if (atomicAdd(&sl.done, (int)c) + (int)c == n) fin |= 1u << s;
-          }
-          emacc[s] = 0;
+        u32 em_s = 0;
+        if (emitted_out) {
+#pragma unroll
+          for (int s2 = 0; s2 < V; ++s2)
+            if (s2 == s) {
+              em_s = emacc[s2];
+              emacc[s2] = 0;
+            }
+        }
+        const u32 es = emitted_out ? __reduce_add_sync(FULL, em_s) : 0u;
+        if (lane == 0) {
+          SlotInfo& sl = S.slot[s];
+          const int n = *(volatile int*)&sl.n;  // read before the count: the slot may then be reloaded
+          if (emitted_out) atomicAdd(&sl.emitted, (unsigned long long)es);
+          __threadfence_block();
+          if (atomicAdd(&sl.done, (int)c) + (int)c == n) fin |= 1u << s;
         }
       }
       fin = __shfl_sync(FULL, fin, 0);
@@ -428,8 +447,13 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       }
       u32 wem = 0;
       Reg* regs = slot_regs<C>(smem_raw, s, k);
+#ifdef GM_WALK_NOINLINE
+      csr_walk(wid, ww, tau, k, wus, wps, DenseFlat{dense}, stamp, scan, prov, regs, wem, z0, b0, mtab,
+               (u32)C::MTAB, wfast);
+#else
       walk_warp<true>(wid, ww, tau, k, wus, wps, dense, stamp, scan, prov, regs, nullptr, wem, z0, b0, mtab,
                       (u32)C::MTAB, nullptr, wfast);
+#endif
       wem = __shfl_sync(FULL, wem, 0);
       GM_STAT(3, lane == 0);  // warp walks
       GM_STAT(4, lane == 0 ? wem : 0u);
