@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
                (u32)C::MTAB, wfast);
 #else
       walk_warp<true>(wid, ww, tau, k, wus, wps, dense, stamp, scan, prov, regs, nullptr, wem, z0, b0, mtab,
-                      (u32)C::MTAB, nullptr, wfast);
+                      (u32)C::MTAB, ltab, wfast);
 #endif
       wem = __shfl_sync(FULL, wem, 0);
       GM_STAT(3, lane == 0);  // warp walks
@@ -483,7 +483,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 #else
       flush_counts();
 #endif
+#ifndef GM_STATS_WALK
       GM_STAT(0, lane == 0);  // idle iterations
+#endif
 #ifdef GM_STATS
     { const long long now = clock64(); if (lane == 0 && t_prev) atomicAdd(&g_stats[t_sec], (unsigned long long)(now - t_prev)); t_prev = now; t_sec = 12; }
 #endif
@@ -542,6 +544,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 #pragma unroll
         for (int s2 = 0; s2 < V; ++s2)
           avail |= ticket_valid(*(volatile unsigned*)&S.slot[s2].grab, *(volatile unsigned*)&S.slot[s2].hdr);
+#ifndef GM_STATS_WALK
         if (lane == 0 && !avail) atomicAdd(&g_stats[7], (unsigned long long)__popc(nn));
         if (lane == 0) {
           atomicAdd(&g_stats[1], 1ull);
@@ -549,6 +552,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
           atomicAdd(&g_stats[5], (unsigned long long)__popc(dp));
           atomicAdd(&g_stats[6], (unsigned long long)__popc(nn));
         }
+#endif
       }
 #endif
       if (live) {

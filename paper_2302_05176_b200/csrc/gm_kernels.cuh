@@ -460,7 +460,8 @@ __global__ void __launch_bounds__(NT)
     const u64 id = surv ? surv[i].id : load_id(ids, i);
     const double w = surv ? surv[i].w : load_w(wts, i);
     walk_warp<false>(id, w, tau, k, useed, pseed, dense, stamp,
-                     scan_all + warp * 32, prov_all + warp * 32, regs, unset_ctr, em);
+                     scan_all + warp * 32, prov_all + warp * 32, regs, unset_ctr, em, 0u, 0.0, nullptr, 0u,
+                     &gm_glog_tab[0][0]);
     if (lane == 0) emitted += em;
   }
   // leave the scratch clean for the next launch

@@ -20,6 +20,7 @@
 #pragma once
 
 #include <type_traits>
+#include <utility>
 
 #include "gm_core.cuh"
 
@@ -106,6 +107,13 @@ struct DenseFlat {
   u32* p;
   __device__ __forceinline__ u32& operator[](u32 i) const { return p[i]; }
 };
+template <class D>
+__device__ __forceinline__ auto dload(const D& d, u32 i) { return d[i]; }
+template <class D, class V>
+__device__ __forceinline__ void dstore(const D& d, u32 i, V v) { d[i] = v; }
+template <class D>
+struct DenseWord { typedef std::remove_cv_t<std::remove_reference_t<decltype(std::declval<D>()[0])>> type; };
+
 struct DenseStrided {  // 128-word rows, `pitch` words apart
   u32* p;
   u32 pitch;
@@ -114,9 +122,9 @@ struct DenseStrided {  // 128-word rows, `pitch` words apart
 
 template <class D>
 __device__ __forceinline__ u32 dget(const D& dense, u32 pos, u32 stamp) {
-  typedef std::remove_cv_t<std::remove_reference_t<decltype(dense[0])>> W;
+  typedef typename DenseWord<D>::type W;
   if (!FyWord<W>::BIG && !GM_OKIF(pos < 65536u, 20u)) return pos + 1;
-  const W e = dense[pos];
+  const W e = dload(dense, pos);
   return (u32)(e >> FyWord<W>::SH) == stamp ? (u32)(e & FyWord<W>::LOW) + 1 : pos + 1;
 }
 
@@ -125,7 +133,7 @@ __device__ __forceinline__ u32 dget(const D& dense, u32 pos, u32 stamp) {
 // permutation entries into `dense`.  scan: 32 doubles, prov: 32 ints (per-warp
 // shared scratch).  mtab: Barrett constants of m = k - z + 1 for z < mtab_n
 // (nullable).  unset_ctr: decremented when a register is first set (nullable).
-// ltab: the log table in shared memory (nullable: the global copy).
+// ltab: the log table (the shared-memory copy in K1, the global one in K2).
 // fast: every spacing divide of the element may use the branch-free divide
 // (w_fast(w)); a run-time flag, so one copy of the walker serves both
 // (kernel code size: the K1 kernel keeps its hot loops in the instruction
@@ -136,15 +144,18 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
                                           int* prov, Reg* regs, int* unset_ctr, u32& emitted,
                                           u32 z_start = 0, double b_start = 0.0,
                                           const u32* mtab = nullptr, u32 mtab_n = 0,
-                                          const double* ltab = nullptr, bool fast = false) {
+                                          const double* ltab = &gm_glog_tab[0][0], bool fast = false) {
   const unsigned FULL = 0xFFFFFFFFu;
   const int lane = threadIdx.x & 31;
   const u64 ubase = useed + id * K_ELEM;
   const u64 pbase = pseed + id * K_ELEM;
   double b = b_start;
   u32 z0 = z_start;
-  typedef std::remove_cv_t<std::remove_reference_t<decltype(dense[0])>> DW;
+  typedef typename DenseWord<D>::type DW;
   while (z0 < k) {
+#ifdef GM_STATS_WALK
+    long long tw0 = clock64();
+#endif
     const u32 z = z0 + lane + 1;
     const bool valid = z <= k;
     // the permutation draws and the dense-array reads first (they do not
@@ -154,15 +165,23 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
     if (valid) j = FyWord<DW>::BIG ? perm_draw_big(pbase, z, k)
                    : (mtab && z < mtab_n) ? perm_draw_m(pbase, z, k, mtab[z]) : perm_draw(pbase, z, k);
     const u32 zi = z - 1, ji = j - 1;
-    u32 vz = valid ? dget(dense, zi, stamp) : 0u;
-    const u32 mj = valid ? dget(dense, ji, stamp) : 0u;
+    // raw words only: they are decoded after the spacings and the prefix, so
+    // the warp does not wait for the loads before its arithmetic
+    DW ez = 0, ej = 0;
+    if (valid && (FyWord<DW>::BIG || GM_OKIF(ji < 65536u, 20u))) {
+      ez = dload(dense, zi);
+      ej = dload(dense, ji);
+    }
     double d = 0.0;
     if (valid) {
       const u64 x = mix64(ubase + (u64)z * K_STEP);
-      const double L = ltab ? -log_pos_t(u_open(x), ltab) : -log_pos(u_open(x));
+      const double L = -log_pos_t(u_open(x), ltab);  // ltab: shared memory (K1) or the global copy (K2)
       const double D = __dmul_rn(w, (double)(k - z + 1));
       d = fast ? ddiv_fast(L, D) : ddiv_ieee(L, D);
     }
+#ifdef GM_STATS_WALK
+    { const long long tw1 = clock64(); if (lane == 0) atomicAdd(&g_stats[5], (unsigned long long)(tw1 - tw0)); tw0 = tw1; }
+#endif
     scan[lane] = d;
     prov[lane] = -1;
     __syncwarp();
@@ -183,7 +202,12 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
       for (int i = 0; i < 16; ++i) s2[i] = v[i];
     }
     __syncwarp();
+#ifdef GM_STATS_WALK
+    { const long long tw1 = clock64(); if (lane == 0) atomicAdd(&g_stats[6], (unsigned long long)(tw1 - tw0)); tw0 = tw1; }
+#endif
     const double t = scan[lane];
+    u32 vz = valid ? ((u32)(ez >> FyWord<DW>::SH) == stamp ? (u32)(ez & FyWord<DW>::LOW) + 1 : zi + 1) : 0u;
+    const u32 mj = valid ? ((u32)(ej >> FyWord<DW>::SH) == stamp ? (u32)(ej & FyWord<DW>::LOW) + 1 : ji + 1) : 0u;
     const u32 stop = __ballot_sync(FULL, !(valid && t <= tau));
     const int n_acc = stop ? __ffs(stop) - 1 : 32;
     const bool acc = lane < n_acc;
@@ -212,11 +236,14 @@ __device__ __forceinline__ void walk_warp(u64 id, double w, double tau, u32 k, u
     const u32 higher = same & ~((2u << lane) - 1u);
     GM_CHECK(!acc || (vj >= 1 && vj <= k && vz >= 1 && vz <= k && ji < k), 3u);
     if (acc && higher == 0 && ji >= z0 + (u32)n_acc && GM_OKIF(ji < k, 21u))
-      dense[ji] = ((DW)stamp << FyWord<DW>::SH) | (DW)(vz - 1);
+      dstore(dense, ji, ((DW)stamp << FyWord<DW>::SH) | (DW)(vz - 1));
     if (acc && GM_OKIF(vj >= 1 && vj <= k, 22u) &&
         reg_min<kSharedRegs>(&regs[vj - 1], (u64)__double_as_longlong(t), id) && unset_ctr)
       atomicSub(unset_ctr, 1);
     emitted += (u32)(n_acc + (n_acc < 32 && z0 + n_acc < k ? 1 : 0));
+#ifdef GM_STATS_WALK
+    { const long long tw1 = clock64(); if (lane == 0) { atomicAdd(&g_stats[7], (unsigned long long)(tw1 - tw0)); atomicAdd(&g_stats[0], 1ull); } }
+#endif
     if (n_acc < 32) break;
     b = __shfl_sync(FULL, t, 31);
     z0 += 32;

@@ -8,11 +8,12 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SO = os.path.join(ROOT, "paper_2302_05176_b200", "libgmsketch_b200_stats.so")
+SO = os.environ.get("GM_STATS_SO") or os.path.join(ROOT, "paper_2302_05176_b200", "libgmsketch_b200_stats.so")
 sys.path.insert(0, ROOT)
 if "--build" in sys.argv or not os.path.exists(SO):
     from paper_2302_05176_b200 import build as b  # noqa: E402
-    cmd = ["nvcc", *b.NVCC_FLAGS, "-DGM_STATS", "-o", SO, *b.SOURCES, "-lcudart", "-ldl"]
+    extra = ["-DGM_STATS_WALK"] if os.environ.get("GM_STATS_WALK") else []
+    cmd = ["nvcc", *b.NVCC_FLAGS, "-DGM_STATS", *extra, "-o", SO, *b.SOURCES, "-lcudart", "-ldl"]
     subprocess.run(cmd, check=True, capture_output=True)
     if "--build" in sys.argv:
         sys.exit(0)
@@ -39,6 +40,9 @@ torch.cuda.synchronize()
 L.gm_stats_read(buf)
 names = ["idle iters", "step iters", "live lane-steps", "warp walks", "warp-walk arrivals", "deep lanes at steps",
          "idle lanes at steps", "  of which no slot had tickets"]
+if os.environ.get("GM_STATS_WALK"):  # walk phases (cycles) instead of the lane categories
+    names = ["walk iterations", "step iters", "live lane-steps", "warp walks", "warp-walk arrivals",
+             "walk cycles: draws, dense reads, spacings", "walk cycles: prefix", "walk cycles: resolve, stores, CAS"]
 for i, nme in enumerate(names):
     print(f"{nme:22s} {buf[i]:>14,d}")
 sec = {8: "finalise", 9: "warp walks", 10: "refill", 12: "exit/idle", 13: "lane steps", 14: "completions"}  # section after each marker
