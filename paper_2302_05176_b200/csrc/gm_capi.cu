@@ -187,7 +187,7 @@ int num_sms() {
 #define GM_MINB 2  // resident CTAs per SM the register budget is sized for
 #endif
 #ifndef GM_VSMALL
-#define GM_VSMALL 4
+#define GM_VSMALL 6
 #endif
 // k <= 4096: 12-bit lane-table words with a generation tag (no table clear
 // per element); larger k: 16-bit words, cleared per element
@@ -199,10 +199,51 @@ int num_sms() {
 #endif
 using CsrDefault = CsrCfg<GM_NT, GM_NB, GM_V, GM_MINB, GM_DEEP_PCT, GM_DRAIN, 12>;
 using CsrLargeK = CsrCfg<256, 16, 2, 2, GM_DEEP_PCT, GM_DRAIN, 16>;
-// k <= 512: four vector slots fit in the shared memory two slots of k = 1024
-// take, so a CTA keeps four (small) vectors in flight -- fewer lanes idle
-// while a slot drains (config 3: 19.4 -> 16.4 ms per batch)
-using CsrSmallK = CsrCfg<GM_NT, GM_NB, GM_VSMALL, GM_MINB, GM_DEEP_PCT, GM_DRAIN, 12>;
+// k <= 1024: draw-log lanes (a bit map of drawn positions + the raw draws
+// instead of a (position, value) table; gm_csr.cuh).  The lane area shrinks to
+// 224 B (k-bit map + 48 logged steps), so two 320-thread CTAs fit per SM (20
+// warps instead of 16; 96 registers per thread, no spills), and an element goes
+// to the warp walker only when its expected depth reaches the log's capacity
+// (measured, config 2: tagged table 0.314 ms; draw log 0.305; with the later
+// hand-over 0.3005; with 320 threads 0.296)
+#ifndef GM_PB_LOG
+#define GM_PB_LOG 10  // (12: the tagged table, for A/B builds)
+#endif
+#ifndef GM_NT_LOG
+#define GM_NT_LOG 320
+#endif
+#ifndef GM_NB_LOG
+#define GM_NB_LOG 12  // logged steps / 4
+#endif
+#ifndef GM_V_LOG
+#define GM_V_LOG GM_V
+#endif
+#ifndef GM_DEEP_PCT_LOG
+#define GM_DEEP_PCT_LOG 100
+#endif
+using CsrLog = CsrCfg<GM_NT_LOG, GM_NB_LOG, GM_V_LOG, GM_MINB, GM_DEEP_PCT_LOG, GM_DRAIN, GM_PB_LOG>;
+// k <= 512: draw-log lanes of 160 B (512-bit map + 48 logged steps) and
+// registers of 8 KB per vector leave room for SIX vector slots and 320 threads
+// per CTA, two CTAs per SM -- the more vectors a CTA keeps in flight, the fewer
+// lanes idle while a slot drains (config 3 per batch: 2 slots 19.4 ms, 4 slots
+// 14.6 ms, 5 slots 13.5 ms, 6 slots 12.98 ms; 7 slots x 288 threads 13.27; 8
+// slots x 256 threads 13.85)
+#ifndef GM_PB_SMALL
+#define GM_PB_SMALL 9
+#endif
+#ifndef GM_NB_SMALL
+#define GM_NB_SMALL 12
+#endif
+#ifndef GM_MINB_SMALL
+#define GM_MINB_SMALL GM_MINB
+#endif
+#ifndef GM_NT_SMALL
+#define GM_NT_SMALL 320
+#endif
+#ifndef GM_DEEP_PCT_SMALL
+#define GM_DEEP_PCT_SMALL 100
+#endif
+using CsrSmallK = CsrCfg<GM_NT_SMALL, GM_NB_SMALL, GM_VSMALL, GM_MINB_SMALL, GM_DEEP_PCT_SMALL, GM_DRAIN, GM_PB_SMALL>;
 // One vector under many seeds (GM_FLAG_ONE_VECTOR, k <= 512): every slot
 // holds the same vector, so a slot's elements outnumber the lanes and two
 // slots keep a 512-thread CTA busy; with few slots, element turnover (the
@@ -218,7 +259,18 @@ using CsrSmallK = CsrCfg<GM_NT, GM_NB, GM_VSMALL, GM_MINB, GM_DEEP_PCT, GM_DRAIN
 #ifndef GM_QCAP_ONE
 #define GM_QCAP_ONE 64
 #endif
-using CsrOneVec = CsrCfg<512, GM_NB, GM_VONE, 1, GM_DEEP_PCT, GM_DRAIN, 12, GM_WQ_ONE, GM_QCAP_ONE>;
+// (draw-log lanes of 128 B -- 512-bit map + 32 logged steps -- leave room for
+// 640 threads: config 1 0.293 -> 0.275 ms; 768 threads at 80 registers: 0.312)
+#ifndef GM_NT_ONE
+#define GM_NT_ONE 640
+#endif
+#ifndef GM_NB_ONE
+#define GM_NB_ONE 8
+#endif
+#ifndef GM_PB_ONE
+#define GM_PB_ONE 9
+#endif
+using CsrOneVec = CsrCfg<GM_NT_ONE, GM_NB_ONE, GM_VONE, 1, GM_DEEP_PCT_LOG, GM_DRAIN, GM_PB_ONE, GM_WQ_ONE, GM_QCAP_ONE>;
 
 template <class C, class IdT, class WT>
 int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k,
@@ -806,6 +858,9 @@ static int csr_dispatch(const void* ids, int id_bits, const void* w, int w_bits,
                                          emitted_out, ws, st, a0)                                                    \
        : small_k ? launch_csr<CsrSmallK, I, W>(ids, w, offsets, n_vec, kk, useed, salt, vseeds, one_vec, y_out,     \
                                              s_out, emitted_out, ws, st, a0)                                         \
+       : kk <= 1024                                                                                                  \
+           ? launch_csr<CsrLog, I, W>(ids, w, offsets, n_vec, kk, useed, salt, vseeds, one_vec, y_out, s_out,       \
+                                      emitted_out, ws, st, a0)                                                       \
        : kk <= CsrDefault::KMAX                                                                                      \
            ? launch_csr<CsrDefault, I, W>(ids, w, offsets, n_vec, kk, useed, salt, vseeds, one_vec, y_out, s_out,   \
                                           emitted_out, ws, st, a0)                                                   \

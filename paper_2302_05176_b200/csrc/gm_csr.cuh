@@ -52,9 +52,11 @@ struct CsrCfg {
   static constexpr int NT = NT_;               // threads per CTA
   static constexpr int NWARP = NT_ / 32;
   static constexpr int MINB = MINB_;           // __launch_bounds__ min blocks
-  static constexpr int NB = NB_;               // buckets per lane table (power of 2)
-  static constexpr int SLOTS = 4 * NB_;        // words per lane table
-  static constexpr int CAPI = SLOTS * 13 / 16; // inserts per element before hand-over
+  static constexpr int NB = NB_;               // buckets per lane table (power of 2); draw-log mode: log words / 2
+  // words per lane: the table, or (draw-log mode) the bit map + the draw log
+  static constexpr int SLOTS = PB_ <= 10 ? (1 << PB_) / 32 + 2 * NB_ : 4 * NB_;
+  // inserts (draw-log mode: logged steps, 4 * NB_) per element before hand-over
+  static constexpr int CAPI = (PB_ <= 10 ? 4 * NB_ : 4 * NB_) * 13 / 16;
   static constexpr int V = V_;                 // vectors in flight per CTA
   static constexpr int U = GM_U;               // lane steps per loop iteration
   static constexpr int MTAB = 256;             // Barrett table entries (z < MTAB)
@@ -67,13 +69,25 @@ struct CsrCfg {
   static constexpr bool GEN = PB_ < 16;
   static constexpr u32 VMASK = (1u << PB_) - 1u;
   static constexpr u32 KMAX = 1u << PB_;       // largest k this configuration serves
+  // PB = 10 (k <= 1024): draw-log mode.  The lane keeps no (position, value)
+  // table: a k-bit map of the positions drawn so far (the first SLOTS / 2
+  // words of the lane's area, bucket-major like the table) and the raw draws
+  // of its steps in order (16-bit entries in the other half, word-major).  A
+  // draw whose bit is clear hits an untouched position (value = position + 1,
+  // the common case: one LDS.32, no probe); a set bit is resolved by tracing
+  // the draw log backwards (log_trace), exactly
+  static constexpr bool LOGM = PB_ <= 10;
+  static constexpr int BMW = (1 << PB_) / 32;  // LOGM: bit-map words per lane (KMAX bits)
+  static constexpr int BMB = (BMW + 3) / 4;    // LOGM: bit-map buckets (4 words each)
+  static constexpr int LOGCAP = 4 * NB_;       // LOGM: logged steps per element (2 per word) before hand-over
+  static_assert(PB_ > 10 || PB_ >= 7, "draw-log mode: whole bit-map buckets");
   // expected depth at which an element goes straight to the warp walker
   static constexpr double kDeep = CAPI * (DEEP_PCT_ / 100.0);
-  static_assert((NB_ & (NB_ - 1)) == 0, "NB must be a power of two");
+  static_assert(PB_ <= 10 || (NB_ & (NB_ - 1)) == 0, "NB must be a power of two");
   static_assert(V_ >= 1 && V_ <= 8, "1..8 slots");
   // per-slot field width of a lane's packed finished-element counts
   static constexpr int FW = V_ <= 4 ? 8 : V_ <= 5 ? 6 : 4;
-  static_assert(PB_ == 12 || PB_ == 16, "12-bit (tagged) or 16-bit lane-table words");
+  static_assert(PB_ <= 10 || PB_ == 12 || PB_ == 16, "draw log, 12-bit (tagged) or 16-bit lane-table words");
 };
 
 constexpr int SLOT_EMPTY = 0, SLOT_ACTIVE = 1;
@@ -86,6 +100,7 @@ struct SlotInfo {
   double deep_w;           // weight at which an element is warp-walked
   unsigned long long emitted;
   u64 useed, pseed;         // the vector's uniform / permutation stream seeds
+  u64 pdelta;               // pseed - useed (an element's permutation base from its uniform base)
   // tickets: grab = (gen << 24) | next element index, hdr = (gen << 24) | n,
   // gen counting the slot's passes.  hdr is published before grab, so a
   // ticket is valid iff its gen matches hdr's and its index is below hdr's n
@@ -296,6 +311,81 @@ __device__ __forceinline__ int lane_step(Lane& L, bool fresh, u32* mytab, const 
   return (L.z >= k || L.t > L.tau) ? 1 : 0;
 }
 
+// ---- draw-log mode (C::LOGM, k <= 1024) --------------------------------------
+// The Fisher-Yates state of steps 1..z is the list of their draws j_1..j_z
+// (0-based positions).  The content of position p (p >= z) after those steps
+// is found by walking the list backwards: a step z' that drew p swapped p's
+// content in from position z' - 1, so the trace continues from there (only
+// earlier steps can have drawn that position); with no such step left the
+// content is still the identity, position + 1.  Equal to LazyPermutation's
+// lookup (randgen.py:146-155), with no value ever stored.
+//
+// lg: the lane's log, word wi at lg[wi * NT], entries 2 wi (low half) and
+// 2 wi + 1 (high half).  n: logged steps.  Returns value - 1.
+template <class C>
+__device__ __noinline__ u32 log_trace(const u32* lg, u32 pos, u32 n) {
+  int i = (int)n - 1;
+  if (i >= 0 && !(i & 1)) {  // a lone low half at the top
+    if ((lg[(i >> 1) * C::NT] & 0xFFFFu) == pos) pos = (u32)i;
+    --i;
+  }
+  for (; i >= 1; i -= 2) {
+    const u32 wv = lg[(i >> 1) * C::NT];
+    if ((wv >> 16) == pos) pos = (u32)i;
+    if ((wv & 0xFFFFu) == pos) pos = (u32)i - 1u;
+  }
+  return pos;
+}
+
+// the lane starts an element: clear the bit map (the log needs no clearing)
+template <class C>
+__device__ __forceinline__ void bm_clear(u32* mybm, u32 k) {
+#pragma unroll
+  for (int b = 0; b < C::BMB; ++b)
+    if ((u32)b * 128u < k) *reinterpret_cast<uint4*>(mybm + b * (C::NT * 4)) = make_uint4(0, 0, 0, 0);
+}
+
+// lane_step in draw-log mode (same contract; 2 = the log is full)
+template <class C>
+__device__ __forceinline__ int lane_step_log(Lane& L, bool fresh, u32* mybm, u32* mylog, const u64* mtab64, u32 k,
+                                             const double* ltab) {
+  const bool acc = !fresh;
+  const u32 zi = L.z, zs = zi + 1;
+  if (acc & (zi >= (u32)C::LOGCAP)) return 2;  // hand over before step zs
+  // permutation draw of step zs and its bit-map word
+  const u64 g = mix64(L.pbase + (u64)zs * K_STEP);
+  const u32 m = k - zs + 1;
+  u32 ji = zi + mod_barrett64(g, m, mtab64[min(zs, (u32)C::MTAB - 1)]);
+  u32* bw = mybm + (ji >> 7) * (C::NT * 4) + ((ji >> 5) & 3u);
+  u32 word = *bw;
+  // next arrival's spacing (independent of this step's permutation work)
+  const u32 zn = acc ? min(zs + 1, k) : 1u;
+  const u64 x = mix64(L.ubase + (u64)zn * K_STEP);
+  const double Lg = -log_pos_t(u_open(x), ltab);
+  const double D = __dmul_rn(L.w, (double)(k - zn + 1));
+  double dq = ddiv_fast(Lg, D);
+  if (!L.fast) dq = ddiv_ieee(Lg, D);
+  const bool redraw = ((u32)(g >> 32) == 0xFFFFFFFFu) | (zs >= (u32)C::MTAB);  // the Barrett draw is not exact
+  u32 vj = ji;  // value - 1
+  if (acc & (redraw | (((word >> (ji & 31u)) & 1u) != 0u))) {
+    if (redraw) {
+      ji = perm_draw(L.pbase, zs, k) - 1;
+      bw = mybm + (ji >> 7) * (C::NT * 4) + ((ji >> 5) & 3u);
+      word = *bw;
+    }
+    vj = ((word >> (ji & 31u)) & 1u) ? log_trace<C>(mylog, ji, zi) : ji;
+  }
+  if (acc) {
+    *bw = word | (1u << (ji & 31u));
+    reinterpret_cast<unsigned short*>(mylog + (zi >> 1) * C::NT)[zi & 1u] = (unsigned short)ji;
+  }
+  reg_min_lane(&L.regs[vj], (u64)__double_as_longlong(L.t), L.id, acc);
+  L.b = acc ? L.t : L.b;
+  L.z = acc ? zs : L.z;
+  L.t = __dadd_rn(L.b, dq);
+  return (L.z >= k || L.t > L.tau) ? 1 : 0;
+}
+
 // ---- vector slots ----------------------------------------------------------
 template <class C>
 __device__ __forceinline__ Reg* slot_regs(unsigned char* smem, int s, u32 k) {
@@ -424,6 +514,7 @@ __device__ __noinline__ void slot_load(CsrShared& S, int s, unsigned char* smem,
       // per-vector seeds (a batch of one vector under many seeds) or the batch's
       sl.useed = vseeds ? vseeds[v] : useed;
       sl.pseed = sl.useed ^ salt;
+      sl.pdelta = sl.pseed - sl.useed;
       sl.fast = Wsum ? (vflags[v] & 1) : fast;
       sl.emitted = 0;
       sl.seq = ++S.seq;

@@ -65,6 +65,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   // floor(2^64 / m) for m = k - z + 1, z < MTAB: the lane step's draw in one 64-bit Barrett reduction
   u64* mtab64 = reinterpret_cast<u64*>(reinterpret_cast<int*>(ltab + 256 + NWARP * 32) + NWARP * 32);
   u32* mytab = tables + tid * 4;
+  // draw-log mode: the lane's bit map of drawn positions is the first part of
+  // its area (bucket-major, at mytab), its draw log the rest (word-major)
+  u32* mylog = tables + (size_t)NT * (C::BMB * 4) + tid;
   // WQ: this warp's staging area (ids, weights of a ticket batch) and queue
   unsigned char* wq_area = reinterpret_cast<unsigned char*>(mtab64 + C::MTAB) + (size_t)warp * (8 + C::WQ * 16 + C::QCAP * 20);
   int* q_pos = reinterpret_cast<int*>(wq_area);  // [0] head, [1] tail: monotone ring positions
@@ -81,7 +84,10 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     mtab64[z] = (z >= 1 && z <= k) ? barrett_magic64(k - z + 1) : 0ull;
   }
   for (u32 i = tid; i < 256; i += NT) ltab[i] = gm_glog_tab[i >> 1][i & 1];
-  tab_clear<C>(mytab);
+  if constexpr (C::LOGM)
+    bm_clear<C>(mytab, C::KMAX);
+  else
+    tab_clear<C>(mytab);
   if (C::WQ > 0 && lane == 0) q_pos[0] = q_pos[1] = 0;
   for (u32 i = lane; i < k; i += 32) dense[i] = 0;  // stamps restart every launch
   if (tid < V) {
@@ -214,7 +220,10 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     if (nx_w >= sl.deep_w) {
       deep = true;
     } else {
-      tab_next_element<C>(mytab, L.g24);
+      if constexpr (C::LOGM)
+        bm_clear<C>(mytab, k);
+      else
+        tab_next_element<C>(mytab, L.g24);
       live = true;
       fresh = true;
     }
@@ -435,7 +444,14 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         __syncwarp();
         stamp = 1;
       }
-      if (wres) {  // the source lane's live table entries -> dense array
+      if (C::LOGM && wres) {  // the source lane's drawn positions, traced to their values -> dense array
+        const u32* slog = tables + (size_t)NT * (C::BMB * 4) + (warp * 32 + src);
+        for (u32 i = lane; i < z0; i += 32) {
+          const u32 pos = (slog[(i >> 1) * NT] >> ((i & 1u) * 16)) & 0xFFFFu;
+          if (pos >= z0) dense[pos] = (stamp << 16) | log_trace<C>(slog, pos, z0);
+        }
+        __syncwarp();
+      } else if (wres) {  // the source lane's live table entries -> dense array
         const u32* stab = tables + (warp * 32 + src) * 4;
         const u32 sg24 = __shfl_sync(FULL, L.g24, src);
         for (u32 wi = lane; wi < (u32)C::SLOTS; wi += 32) {
@@ -556,7 +572,11 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       }
 #endif
       if (live) {
-        const int rc = lane_step<C>(L, fresh, mytab, mtab64, k, ltab);
+        int rc;
+        if constexpr (C::LOGM)
+          rc = lane_step_log<C>(L, fresh, mytab, mylog, mtab64, k, ltab);
+        else
+          rc = lane_step<C>(L, fresh, mytab, mtab64, k, ltab);
         fresh = false;
         if (rc == 1) {
           em += L.z < k ? L.z + 1 : L.z;

@@ -227,6 +227,35 @@ def test_config2_full_vs_oracle():
     assert m.tolist() == np.sum(so[0::2] == so[1::2], axis=1).tolist()
 
 
+@pytest.mark.parametrize("k,depth", [(1024, 36.0), (1024, 44.0), (512, 36.0), (300, 30.0), (40, 12.0), (8, 3.0)])
+def test_draw_log_lanes_traces_and_handovers(k, depth):
+    """K1's draw-log lanes (k <= 1024): vectors of near-equal weights sized
+    so that every element is walked by a lane to about `depth` steps --
+    repeated draws resolved by tracing the log (frequent at small k), logs
+    that fill up and hand the element to the warp walker (depths near the
+    48-step capacity) -- bit for bit against the oracle."""
+    rng = np.random.default_rng(k * 1000 + int(depth))
+    n0 = max(2, int(k * (math.log(k) + 2.5) / depth))
+    sizes = rng.integers(max(1, int(n0 * 0.8)), int(n0 * 1.2) + 2, size=48)
+    off = np.zeros(sizes.size + 1, np.int64)
+    off[1:] = np.cumsum(sizes)
+    ids = np.concatenate([rng.choice(1 << 31, size=int(m), replace=False) + 1 for m in sizes]).astype(np.uint32)
+    w = rng.uniform(0.7, 1.3, size=int(off[-1]))
+    y, s = batch_np(gm.sketch_csr(ids, w, off, k, gm.SeedScheme(77)))
+    rc, yo, so, _ = O.sketch_csr(ids.astype(np.uint64), w, off, k, 77, mode=0, threads=8)
+    assert rc == 0
+    assert_regs(y, s, yo, so)
+    if k <= 512:  # one vector under many seeds (the 640-thread shape, 32-step logs)
+        schemes = [gm.SeedScheme(500 + r) for r in range(12)]
+        lo, hi = int(off[3]), int(off[4])
+        b1 = gm.sketch_vector_seeds(ids[lo:hi], w[lo:hi], k, schemes)
+        y1, s1 = batch_np(b1)
+        for r in (0, 5, 11):
+            rc, yo1, so1, _, _ = O.sketch_stream(ids[lo:hi].astype(np.uint64), w[lo:hi], k, 500 + r)
+            assert rc == 0
+            assert_regs(y1[r], s1[r], yo1, so1)
+
+
 def test_config3_subset_vs_oracle():
     ids, w, off, k, seed = workloads.config3(n_vectors=3000)
     y, s = batch_np(gm.sketch_csr(ids, w, off, k, gm.SeedScheme(seed)))
