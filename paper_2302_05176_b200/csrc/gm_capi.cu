@@ -272,11 +272,11 @@ using CsrSmallK = CsrCfg<GM_NT_SMALL, GM_NB_SMALL, GM_VSMALL, GM_MINB_SMALL, GM_
 #endif
 using CsrOneVec = CsrCfg<GM_NT_ONE, GM_NB_ONE, GM_VONE, 1, GM_DEEP_PCT_LOG, GM_DRAIN, GM_PB_ONE, GM_WQ_ONE, GM_QCAP_ONE>;
 
-template <class C, class IdT, class WT>
-int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k,
+template <class C, class IdT, class WT, bool kCount>
+int launch_csr_t(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k,
                u64 useed, u64 salt, const u64* vseeds, int one_vec, double* y, u64* s, int64_t* em, Workspace* ws,
                cudaStream_t st, int attempt0) {
-  auto kern = csr4_kernel<C, IdT, WT>;
+  auto kern = csr4_kernel<C, IdT, WT, kCount>;
   const size_t smem = csr_smem_bytes<C>(k);
   int per_sm = 0;
   {
@@ -321,6 +321,16 @@ int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n
                                             attempt0, nullptr);
   CK(cudaGetLastError());
   return GM_OK;
+}
+
+template <class C, class IdT, class WT>
+int launch_csr(const void* ids, const void* w, const int64_t* offsets, int64_t n_vec, u32 k,
+               u64 useed, u64 salt, const u64* vseeds, int one_vec, double* y, u64* s, int64_t* em, Workspace* ws,
+               cudaStream_t st, int attempt0) {
+  return em ? launch_csr_t<C, IdT, WT, true>(ids, w, offsets, n_vec, k, useed, salt, vseeds, one_vec, y, s, em, ws, st,
+                                            attempt0)
+            : launch_csr_t<C, IdT, WT, false>(ids, w, offsets, n_vec, k, useed, salt, vseeds, one_vec, y, s, em, ws, st,
+                                             attempt0);
 }
 
 int check_common(int id_bits, int w_bits, int32_t k) {

@@ -337,12 +337,13 @@ __device__ __noinline__ u32 log_trace(const u32* lg, u32 pos, u32 n) {
   return pos;
 }
 
-// the lane starts an element: clear the bit map (the log needs no clearing)
+// the lane starts an element: clear the bit map (the log needs no clearing).
+// All of the configuration's buckets, whatever k: unconditional stores are
+// cheaper than a predicate per bucket.
 template <class C>
-__device__ __forceinline__ void bm_clear(u32* mybm, u32 k) {
+__device__ __forceinline__ void bm_clear(u32* mybm) {
 #pragma unroll
-  for (int b = 0; b < C::BMB; ++b)
-    if ((u32)b * 128u < k) *reinterpret_cast<uint4*>(mybm + b * (C::NT * 4)) = make_uint4(0, 0, 0, 0);
+  for (int b = 0; b < C::BMB; ++b) *reinterpret_cast<uint4*>(mybm + b * (C::NT * 4)) = make_uint4(0, 0, 0, 0);
 }
 
 // lane_step in draw-log mode (same contract; 2 = the log is full)

@@ -40,7 +40,9 @@ __device__ __noinline__ void csr_walk(u64 id, double w, double tau, u32 k, u64 u
 
 // Dynamic shared memory: Reg regs[V][k] | u32 tables[NB][NT][4] | u32 mtab[MTAB]
 //   | double scan[NWARP][32] | int prov[NWARP][32]
-template <class C, class IdT, class WT>
+// kCount: the caller asked for the per-vector arrival counts (emitted_out);
+// the uncounted instantiation carries no count registers or instructions
+template <class C, class IdT, class WT, bool kCount>
 __global__ void __launch_bounds__(C::NT, C::MINB)
     csr4_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts,
                 const int64_t* __restrict__ offsets, int64_t n_vec, u32 k, u64 useed, u64 salt,
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   }
   for (u32 i = tid; i < 256; i += NT) ltab[i] = gm_glog_tab[i >> 1][i & 1];
   if constexpr (C::LOGM)
-    bm_clear<C>(mytab, C::KMAX);
+    bm_clear<C>(mytab);
   else
     tab_clear<C>(mytab);
   if (C::WQ > 0 && lane == 0) q_pos[0] = q_pos[1] = 0;
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     if (lane == 0) {
       SlotInfo& sl = S.slot[s];
       const int n = *(volatile int*)&sl.n;
-      if (emitted_out) atomicAdd(&sl.emitted, em_sum);
+      if (kCount) atomicAdd(&sl.emitted, em_sum);
       __threadfence_block();
       const int old = atomicAdd(&sl.done, c);
       if (old + c == n) fin |= 1u << s;
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       deep = true;
     } else {
       if constexpr (C::LOGM)
-        bm_clear<C>(mytab, k);
+        bm_clear<C>(mytab);
       else
         tab_next_element<C>(mytab, L.g24);
       live = true;
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   // end of the round)
   auto finish_element = [&]() {
     dpack += 1u << (C::FW * L.slot);
-    if (emitted_out) {
+    if constexpr (kCount) {
 #pragma unroll
       for (int s = 0; s < V; ++s) emacc[s] += L.slot == s ? em : 0u;
     }
@@ -252,7 +254,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         const int s = (int)live_s;
         const u32 c = __reduce_add_sync(FULL, (dpack >> (C::FW * s)) & FM);
         u32 em_s = 0;
-        if (emitted_out) {
+        if constexpr (kCount) {
 #pragma unroll
           for (int s2 = 0; s2 < V; ++s2)
             if (s2 == s) {
@@ -260,11 +262,11 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
               emacc[s2] = 0;
             }
         }
-        const u32 es = emitted_out ? __reduce_add_sync(FULL, em_s) : 0u;
+        const u32 es = kCount ? __reduce_add_sync(FULL, em_s) : 0u;
         if (lane == 0) {
           SlotInfo& sl = S.slot[s];
           const int n = *(volatile int*)&sl.n;  // read before the count: the slot may then be reloaded
-          if (emitted_out) atomicAdd(&sl.emitted, (unsigned long long)es);
+          if (kCount) atomicAdd(&sl.emitted, (unsigned long long)es);
           __threadfence_block();
           if (atomicAdd(&sl.done, (int)c) + (int)c == n) fin |= 1u << s;
         }
@@ -309,7 +311,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         skips += sk ? 1u : 0u;
       }
       dpack += skips << (C::FW * b_slot);
-      if (emitted_out) {
+      if constexpr (kCount) {
 #pragma unroll
         for (int s2 = 0; s2 < V; ++s2) emacc[s2] += b_slot == s2 ? skips : 0u;
       }
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         y_out[v * (int64_t)k + j] = __longlong_as_double((long long)rg.y);
         s_out[v * (int64_t)k + j] = rg.id;
       }
-      if (emitted_out && lane == 0) emitted_out[v] = (int64_t)sl.emitted;
+      if (kCount && lane == 0) emitted_out[v] = (int64_t)sl.emitted;
       if (lane == 0)
         GM_TRACE((unsigned long long)(v & 0xFFFFFFFF) | ((unsigned long long)att << 32) | (1ull << 40) |
                  ((unsigned long long)blockIdx.x << 48) | ((unsigned long long)s << 60));
@@ -437,7 +439,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       const u32 z0 = wres ? __shfl_sync(FULL, L.z, src) : 0u;
       const double b0 = wres ? __shfl_sync(FULL, L.b, src) : 0.0;
       const bool wfast = __shfl_sync(FULL, (int)L.fast, src) != 0;
-      const u32 em0 = __shfl_sync(FULL, em, src);
+      const u32 em0 = kCount ? __shfl_sync(FULL, em, src) : 0u;
       const u64 wus = *(volatile u64*)&S.slot[s].useed, wps = *(volatile u64*)&S.slot[s].pseed;
       if (++stamp > 0xFFFFu) {
         for (u32 i = lane; i < k; i += 32) dense[i] = 0;
@@ -579,12 +581,12 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
           rc = lane_step<C>(L, fresh, mytab, mtab64, k, ltab);
         fresh = false;
         if (rc == 1) {
-          em += L.z < k ? L.z + 1 : L.z;
+          if (kCount) em += L.z < k ? L.z + 1 : L.z;
           live = false;
           finish_element();
           if (nx_ok) start_next();
         } else if (rc == 2) {
-          em += L.z;
+          if (kCount) em += L.z;
           live = false;
           deep = true;
           resume = true;
