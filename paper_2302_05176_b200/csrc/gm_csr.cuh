@@ -105,7 +105,7 @@ struct SlotInfo {
   // gen counting the slot's passes.  hdr is published before grab, so a
   // ticket is valid iff its gen matches hdr's and its index is below hdr's n
   // (a ticket of an earlier pass can never validate against a later header)
-  unsigned grab;
+  alignas(8) unsigned grab;  // (grab, hdr): one 8-byte load
   unsigned hdr;
   unsigned gen;
   int n;                   // elements
@@ -119,6 +119,7 @@ struct SlotInfo {
 struct CsrShared {
   SlotInfo slot[8];
   unsigned seq;
+  int cur;                  // the slot lanes take tickets from first (a hint, see take_next)
   // one vector under many seeds: its weight sum, divide range and validity
   // are the same for every sketch -- computed by the first slot load, reused
   double one_W;

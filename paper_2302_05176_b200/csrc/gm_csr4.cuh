@@ -27,6 +27,18 @@
 
 namespace gmk {
 
+// lane steps per scheduling round, by the batch's expected arrivals per
+// element (see u_run)
+#ifndef GM_URUN0
+#define GM_URUN0 2
+#endif
+#ifndef GM_URUN1
+#define GM_URUN1 4
+#endif
+#ifndef GM_URUN2
+#define GM_URUN2 6
+#endif
+
 #ifdef GM_WALK_NOINLINE
 // the warp walker as a call (kernel code size)
 template <class D>
@@ -102,6 +114,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
   }
   if (tid == 0) {
     S.seq = 0;
+    S.cur = 0;
     S.one_state = 0;
   }
   __syncthreads();
@@ -132,7 +145,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     const float n_avg = one_vec ? (float)(offsets[1] - offsets[0])
                                 : (float)(offsets[n_vec] - offsets[0]) / (float)n_vec;
     const float depth = (float)k * (__logf((float)k) + 2.5f) / fmaxf(n_avg, 1.0f);
-    u_run = depth < 2.0f ? 2 : depth < 6.0f ? 4 : 6;
+    u_run = depth < 2.0f ? GM_URUN0 : depth < 6.0f ? GM_URUN1 : GM_URUN2;
   }
   // the lane's next element, taken and loading while the current one is walked
   bool nx_ok = false;
@@ -180,19 +193,28 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
       nx_ok = true;
       return;
     }
-    int best = -1;
-    unsigned bseq = 0xFFFFFFFFu;
+    // the slot the CTA is currently handing out (a hint: one 8-byte load
+    // instead of the scan over all the slots; rescanned -- oldest slot with
+    // untaken elements first -- when it has run dry)
+    int best = *(volatile int*)&S.cur;
+    {
+      const unsigned long long gh = *(volatile unsigned long long*)&S.slot[best].grab;  // (grab, hdr)
+      if (!ticket_valid((unsigned)gh, (unsigned)(gh >> 32))) {
+        best = -1;
+        unsigned bseq = 0xFFFFFFFFu;
 #pragma unroll
-    for (int s = 0; s < V; ++s) {
-      const unsigned g = *(volatile unsigned*)&S.slot[s].grab;
-      const unsigned h = *(volatile unsigned*)&S.slot[s].hdr;
-      const unsigned q = *(volatile unsigned*)&S.slot[s].seq;
-      if (ticket_valid(g, h) && q < bseq) {
-        bseq = q;
-        best = s;
+        for (int s = 0; s < V; ++s) {
+          const unsigned long long gh2 = *(volatile unsigned long long*)&S.slot[s].grab;
+          const unsigned q = *(volatile unsigned*)&S.slot[s].seq;
+          if (ticket_valid((unsigned)gh2, (unsigned)(gh2 >> 32)) && q < bseq) {
+            bseq = q;
+            best = s;
+          }
+        }
+        if (best < 0) return;
+        *(volatile int*)&S.cur = best;
       }
     }
-    if (best < 0) return;
     const unsigned t = atomicAdd(&S.slot[best].grab, 1u);
     __threadfence_block();
     if (!ticket_valid(t, *(volatile unsigned*)&S.slot[best].hdr)) return;  // ran dry meanwhile
