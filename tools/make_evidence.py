@@ -88,6 +88,8 @@ def main():
         ev["probe_warp_inst_per_arrival"] = p["warp_inst_per_arrival"]
         ev["probe_pipes"] = p["pipes_pct"]
     csr = [n for n in last if n.startswith("csr3_kernel") or n.startswith("csr4_kernel")]
+    # the uncounted instantiation (kCount = 0: what bench.py times) before the counted one
+    csr.sort(key=lambda n: not n.rstrip().endswith(", 0>"))
     if csr:
         e = ev["kernels"][csr[0]]
         ev["kernel"] = csr[0]
