@@ -358,6 +358,7 @@ __device__ __forceinline__ int lane_step_log(Lane& L, bool fresh, u32* mybm, u32
   const u64 g = mix64(L.pbase + (u64)zs * K_STEP);
   const u32 m = k - zs + 1;
   u32 ji = zi + mod_barrett64(g, m, mtab64[min(zs, (u32)C::MTAB - 1)]);
+  GM_CHECK(ji < k && k <= C::KMAX && zi < k, 30u);
   u32* bw = mybm + (ji >> 7) * (C::NT * 4) + ((ji >> 5) & 3u);
   u32 word = *bw;
   // next arrival's spacing (independent of this step's permutation work)
@@ -377,6 +378,7 @@ __device__ __forceinline__ int lane_step_log(Lane& L, bool fresh, u32* mybm, u32
     }
     vj = ((word >> (ji & 31u)) & 1u) ? log_trace<C>(mylog, ji, zi) : ji;
   }
+  GM_CHECK(!acc || (ji < k && vj < k && zi < (u32)C::LOGCAP), 31u);
   if (acc) {
     *bw = word | (1u << (ji & 31u));
     reinterpret_cast<unsigned short*>(mylog + (zi >> 1) * C::NT)[zi & 1u] = (unsigned short)ji;

@@ -472,6 +472,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         const u32* slog = tables + (size_t)NT * (C::BMB * 4) + (warp * 32 + src);
         for (u32 i = lane; i < z0; i += 32) {
           const u32 pos = (slog[(i >> 1) * NT] >> ((i & 1u) * 16)) & 0xFFFFu;
+          GM_CHECK(pos < k && z0 <= (u32)C::LOGCAP, 32u);
           if (pos >= z0) dense[pos] = (stamp << 16) | log_trace<C>(slog, pos, z0);
         }
         __syncwarp();
