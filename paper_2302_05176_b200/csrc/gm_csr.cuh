@@ -7,18 +7,21 @@
 // randgen.py:158-207) is folded into the k registers; a pass that leaves a
 // register unset is repeated with a larger tau.
 //
-// Lane walker (lane_step): one lane walks one element, one queue step per
-// call (straight-line step: the next spacing, the permutation draw, both
-// table probes, the register read; rare cases take a slow path).  An element
-// whose expected depth k*w*tau is large, or whose lane table fills up, is
-// walked by the whole warp in-line (walk_warp, 32 steps per iteration).
+// Lane walker: one lane walks one element, one queue step per call
+// (straight-line step: the next spacing, the permutation draw, the lane's
+// Fisher-Yates lookup, the register read; rare cases take a slow path).
+// k <= 1024: lane_step_log, the lane's Fisher-Yates state is its draw log and
+// a bit map of drawn positions (below); larger k: lane_step, a per-lane
+// (position, value) table.  An element whose expected depth k*w*tau is
+// large, or whose log / table fills up, is walked by the whole warp in-line
+// (walk_warp, 32 steps per iteration).
 //
 // Vector slots: the CTA keeps V vectors in flight (k registers in shared
 // memory + a header, SlotInfo); slot_load takes the next vector of the batch
 // into a slot (its weight sum, validation and divide-range check in the same
 // warp pass), slot_open_pass (re)opens a pass with its tau.
 //
-// Lane permutation table (LazyPermutation, randgen.py:146-155): NB buckets of
+// Lane permutation table (k > 1024; LazyPermutation, randgen.py:146-155): NB buckets of
 // 4 words per lane, open addressing with bucket-linear probing, cleared when
 // the lane takes an element; a word is (position << 16) | (value - 1), 0 =
 // empty (a stored position is some j - 1 >= z >= 1).  Entries are never

@@ -8,13 +8,14 @@
 // NEXT element taken and loading (id, weight from HBM/L2) while it walks the
 // current one, so a lane whose element ends goes on with the next one at the
 // next step, with no warp-wide hand-out and no idle steps.  A lane starting
-// an element retires its table by bumping a generation tag (k <= 4096), and
+// an element clears its bit map of drawn positions (k <= 1024, draw-log lanes)
+// or retires its table by bumping a generation tag (k <= 4096), and
 // finished elements are counted per warp at the end of each round of lane
 // steps (one atomic per slot, the register updates fenced first); the warp
 // whose count completes a slot finalises it:
 // every register set -> write the sketch out and load the next vector; else
 // reopen the slot for the next pass with a larger tau.  Deep elements and
-// elements whose lane table fills up are walked by the whole warp (walk_warp).
+// elements whose draw log / lane table fills up are walked by the whole warp (walk_warp).
 // Lane steps run in rounds of u_run steps between the warp-level checks
 // (2 / 4 / 6 from the batch's expected arrivals per element).
 //
