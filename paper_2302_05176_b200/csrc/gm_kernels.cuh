@@ -210,7 +210,11 @@ struct __align__(16) Surv {
 // id into the CTA's id set (first sightings only), one atomic per step for
 // the list position.  Per-element work at the moment an element is kept would
 // run at 1/32 of the warp's width (lanes hold kept elements one at a time).
-constexpr int WBUF = 256;
+#ifndef GM_WBUF
+#define GM_WBUF 64
+#endif
+constexpr int WBUF = GM_WBUF;  // per warp; the filter runs ~4% faster on config 4 with 64 than with 256 entries
+static_assert(WBUF >= 32 && WBUF % 8 == 0, "staging area: at least one element per lane, whole lane groups");
 
 __device__ __noinline__ void flush_kept(const Surv* wbuf, u32 wcount, Surv* list, int64_t cap,
                                         unsigned long long* count, unsigned long long* cache) {
@@ -269,6 +273,25 @@ __device__ __forceinline__ u32 stage_kept(u32 keep, const u64 (&idv)[NE], const 
   if (wcount + total > (u32)WBUF) {
     flush_kept(wbuf, wcount, list, cap, count, cache);
     wcount = 0;
+  }
+  if (32 * NE > WBUF && total > (u32)WBUF) {
+    // more kept elements in one iteration than the staging area holds (a
+    // stream in which nearly everything is kept): stage and flush the lanes
+    // in groups of WBUF / NE, each group at most WBUF elements
+    constexpr int G = WBUF / NE;
+    for (int g = 0; g < 32; g += G) {
+      const u32 base = __shfl_sync(0xFFFFFFFFu, incl - c, g);
+      const u32 cnt = __shfl_sync(0xFFFFFFFFu, incl, g + G - 1 < 31 ? g + G - 1 : 31) - base;
+      if (lane >= g && lane < g + G) {
+        u32 p2 = incl - c - base;
+        for (u32 m = keep; m; m &= m - 1, ++p2) {
+          const int e = __ffs(m) - 1;
+          wbuf[p2] = Surv{pick(idv, e), (double)pick(wv, e)};
+        }
+      }
+      flush_kept(wbuf, cnt, list, cap, count, cache);
+    }
+    return 0;
   }
   u32 pos = wcount + incl - c;
   for (u32 m = keep; m; m &= m - 1, ++pos) {

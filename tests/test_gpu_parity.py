@@ -976,6 +976,24 @@ def test_elements_bad_weight_anywhere_raises(bad, id_dtype):
         gm.sketch_elements(ids, w, 1024, gm.SeedScheme(3))
 
 
+@pytest.mark.parametrize("n,k,nd", [(200_000, 4096, 50), (500_000, 8192, 2000), (100_000, 64, 100_000),
+                                    (300_000, 4096, 300)])
+def test_elements_streams_where_nearly_everything_is_kept(n, k, nd):
+    """K2 filter with few distinct heavy keys (every occurrence passes the
+    first-arrival test): whole warps keep all eight of their elements in one
+    iteration, more than the per-warp staging area holds -- the grouped
+    staging path -- and streams of all-distinct ids with k small."""
+    rng = np.random.default_rng(n + k)
+    keys = rng.choice(1 << 62, size=nd, replace=False).astype(np.uint64) + np.uint64(1)
+    kw = rng.uniform(0.5, 2.0, size=nd).astype(np.float32)
+    idx = rng.integers(0, nd, size=n)
+    ids, w = keys[idx], kw[idx]
+    y, s, _ = gm.sketch_elements(ids, w, k, gm.SeedScheme(11))
+    rc, yo, so, _, _ = O.sketch_stream(ids, w.astype(np.float64), k, 11)
+    assert rc == 0
+    assert_regs(y.cpu().numpy(), s.cpu().numpy().view(np.uint64), yo, so)
+
+
 @pytest.mark.parametrize("n", [1, 3, 100, 1000, 5000])
 @pytest.mark.parametrize("k", [1, 2, 64, 4096])
 def test_elements_small_sets_with_repeats(n, k):
