@@ -179,10 +179,13 @@ __device__ __forceinline__ float filter_x(WT w, float tkf, double tk) {
 // drops a kept element whose id sits in its home slot with one shared load
 // (a hot key already listed: no call, no atomic); first sightings insert
 // (open addressing, 8 probes, then the id is simply listed again).
-constexpr int SURV_CACHE = 1024;
+#ifndef GM_SURV_BITS
+#define GM_SURV_BITS 10
+#endif
+constexpr int SURV_CACHE = 1 << GM_SURV_BITS;
 
 __device__ __forceinline__ u32 surv_slot(u64 id) {
-  return (((u32)(id >> 32) * 0x9E3779B1u) ^ ((u32)id * 0x85EBCA6Bu)) >> 22;  // 10 bits
+  return (((u32)(id >> 32) * 0x9E3779B1u) ^ ((u32)id * 0x85EBCA6Bu)) >> (32 - GM_SURV_BITS);
 }
 
 __device__ __forceinline__ bool surv_cache_first(unsigned long long* cache, u32 h, u64 id) {
