@@ -404,7 +404,7 @@ int run_elements(const void* ids, const void* w, int64_t n, u32 k, u64 useed, u6
     static const bool fused_only = getenv("GM_ELEM_FUSED") && atoi(getenv("GM_ELEM_FUSED")) == 1;
     const int64_t surv_cap = std::min<int64_t>(n, (int64_t)1 << 26);
     if ((rc = grow(&ws->surv, &ws->surv_cap, (size_t)surv_cap, st))) return rc;
-    const int64_t fgrid = std::min<int64_t>((n / 4 + 2 * NT - 1) / (2 * NT) + 1, (int64_t)num_sms() * 8);
+    const int64_t fgrid = std::min<int64_t>((n / 4 + 2 * NT - 1) / (2 * NT) + 1, (int64_t)num_sms() * 2 * filter_minb<IdT, WT>());
     int surv_per_sm = 0;  // the list walk is latency-bound: as many resident CTAs as fit
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&surv_per_sm, elem_survivor_kernel<W>, NT, 0));
     surv_per_sm = std::max(surv_per_sm, 1);

@@ -304,8 +304,14 @@ __device__ __forceinline__ u32 stage_kept(u32 keep, const u64 (&idv)[NE], const 
   return wcount + total;
 }
 
+// resident CTAs per SM the filter's register budget is sized for: 5 with
+// 32-bit ids and fp32 weights (48 registers, no spills; config 5 1.317 ->
+// 1.300 ms), 4 otherwise (64-bit ids need 64 registers: 5 CTAs spill and run
+// config 4 8% slower, 3 CTAs 12%)
 template <class IdT, class WT>
-__global__ void __launch_bounds__(NT, 4)
+constexpr int filter_minb() { return sizeof(IdT) == 4 && sizeof(WT) == 4 ? 5 : 4; }
+template <class IdT, class WT>
+__global__ void __launch_bounds__(NT, filter_minb<IdT, WT>())
     elem_filter_kernel(const IdT* __restrict__ ids, const WT* __restrict__ wts, int64_t n, u32 k, u64 useed,
                        const double* __restrict__ tau_hi_p, Surv* __restrict__ list, int64_t cap,
                        unsigned long long* count, unsigned long long* emitted_total, unsigned long long* err) {
