@@ -305,8 +305,8 @@ __device__ __forceinline__ u32 stage_kept(u32 keep, const u64 (&idv)[NE], const 
 }
 
 // resident CTAs per SM the filter's register budget is sized for: 5 with
-// 32-bit ids and fp32 weights (48 registers, no spills; config 5 1.317 ->
-// 1.300 ms), 4 otherwise (64-bit ids need 64 registers: 5 CTAs spill and run
+// 32-bit ids and fp32 weights (48 registers and a 24-byte spill; config 5
+// 1.317 -> 1.300 ms), 4 otherwise (64-bit ids need 64 registers: 5 CTAs spill and run
 // config 4 8% slower, 3 CTAs 12%)
 template <class IdT, class WT>
 constexpr int filter_minb() { return sizeof(IdT) == 4 && sizeof(WT) == 4 ? 5 : 4; }
